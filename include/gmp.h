@@ -1,0 +1,184 @@
+/*
+ * gmp.h - C-ABI of libgmp.so, the B200 (sm_100a) g-SpMM / g-SDDMM /
+ * edge_softmax engine.
+ *
+ * Every entry point replaces one function of the reference package's kernel
+ * engine (graphmp 0.1.0, /root/reference/pkg/src/graphmp). The reference is
+ * pure Python with no FFI, so the "binding" a maintainer adds is the ctypes
+ * stub in INTEGRATION.md; paper_1909_01315_b200/_lib.py is that stub.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers; sizes/strides are in elements.
+ *  - Outputs are caller-allocated (the paper's framework-allocates-outputs
+ *    contract); the library never allocates device memory
+ *    except inside gmp_build_schedule's caller-supplied workspace.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ *    stream-ordered and asynchronous; the host syncs only to read err slots.
+ *  - Return value: GMP_OK (0) or an error code; gmp_last_error() returns a
+ *    thread_local detail string for the last failing call on this thread.
+ *  - Feature dtype: GMP_F32 or GMP_F64 (messages and sum/mean/dot
+ *    accumulation are always carried out in fp64).
+ *  - Edge count m must be < 2^31 (int32 indices / edge ids on device).
+ */
+#ifndef GMP_H_
+#define GMP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+enum { GMP_OK = 0, GMP_EINVAL = 1, GMP_ECUDA = 2, GMP_EUNSUPPORTED = 3 };
+
+/* message ops: kernels.py:43 OPS ("copy_lhs","copy_rhs","add","sub","mul","div","dot") */
+enum { GMP_COPY_LHS = 0, GMP_COPY_RHS = 1, GMP_ADD = 2, GMP_SUB = 3,
+       GMP_MUL = 4, GMP_DIV = 5, GMP_DOT = 6 };
+/* operand targets: kernels.py:44 TARGETS ("src","dst","edge"); NONE for copy's unused side */
+enum { GMP_NONE = -1, GMP_SRC = 0, GMP_DST = 1, GMP_EDGE = 2 };
+/* reducers: kernels.py:45 REDUCERS ("sum","max","min","mean") */
+enum { GMP_SUM = 0, GMP_MAX = 1, GMP_MIN = 2, GMP_MEAN = 3 };
+/* feature dtypes */
+enum { GMP_F32 = 0, GMP_F64 = 1 };
+
+/* One grouped index (graph.py:23-32 Adjacency): for CSC (in-adjacency,
+ * graph.py:137) rows are destinations and `indices` are sources; for the
+ * reverse graph's CSC (== forward CSR, graph.py:203-215) rows are sources.
+ * Within a row, indices ascend and parallel edges break ties by edge id. */
+typedef struct {
+  int64_t n_rows;          /* groups (num_nodes) */
+  int64_t m;               /* edges */
+  const int64_t* indptr;   /* n_rows + 1 */
+  const int32_t* indices;  /* m: neighbour node id */
+  const int32_t* eids;     /* m: edge id */
+} gmp_adj;
+
+/* Degree-binned row schedule for an adjacency (built by gmp_build_schedule).
+ * order: row ids sorted by degree, descending (stable). Rows order[0..n_heavy)
+ * have degree > heavy_threshold and are reduced by a whole CTA; the rest by
+ * one warp each. order == NULL means identity order and no CTA rows. */
+typedef struct {
+  const int32_t* order;
+  int64_t n_heavy;
+  int64_t n_nonempty;
+  int32_t heavy_threshold;
+} gmp_sched;
+
+/* COO edge list in edge-id order (graph.py:98-100). */
+typedef struct {
+  int64_t n_nodes;
+  int64_t m;
+  const int32_t* src;
+  const int32_t* dst;
+} gmp_coo;
+
+/* One operand matrix: rows keyed by its target, row-major with leading
+ * dimension ld (elements). dim == 1 with d_out > 1 broadcasts (kernels.py:247-251). */
+typedef struct {
+  const void* data;
+  int64_t ld;
+  int32_t dim;
+  int32_t target; /* GMP_SRC / GMP_DST / GMP_EDGE */
+} gmp_operand;
+
+/* Tunables; pass NULL for defaults. tile_cols = column-tile width of the
+ * row kernels (0 = auto: sized so one column slice of the gathered operand
+ * stays L2-resident - the reference's feature_parallel split, kernels.py:485-513). */
+typedef struct {
+  int32_t tile_cols;
+  int32_t warps_per_cta;
+  int32_t l2_budget_mb;
+} gmp_tuning;
+
+/* ---- schedule ---------------------------------------------------------- */
+
+/* Workspace bytes gmp_build_schedule needs for an n_rows adjacency. */
+size_t gmp_schedule_workspace_size(int64_t n_rows);
+
+/* Sort rows by in-degree (descending, stable) into order_out (n_rows int32,
+ * device) and report the heavy/non-empty prefix lengths into *sched_out
+ * (synchronises `stream` to read them back). Replaces nothing in the
+ * reference (its _GroupedWalk.run walks rows in id order, kernels.py:361-373);
+ * this is the degree-binned scheduling of the north star. */
+int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold,
+                       int32_t* order_out, void* workspace, size_t workspace_bytes,
+                       gmp_sched* sched_out, void* stream);
+
+/* ---- g-SpMM -------------------------------------------------------------
+ * Replaces kernels.gspmm (kernels.py:685-725) with its default strategy
+ * node_parallel (_gspmm_node_parallel + _GroupedWalk, kernels.py:340-482):
+ *   Z[v] = rho_{(u,e,v) in adj row v} phi(lhs, rhs)
+ * op/lhs/rhs follow MessageFunc (kernels.py:72-104): copy_lhs reads lhs only,
+ * copy_rhs reads rhs only; the unused operand has target GMP_NONE.
+ * Z: (n_rows, d_out) row-major with ldz. arg (max/min only, else NULL):
+ * (n_rows, d_out) int64, ld = d_out, the winning edge id, ties -> smallest
+ * edge id, -1 for empty rows (ArgExtrema, kernels.py:147-154). Empty rows get
+ * Z = 0. Mean divides by in-degree (0/0 -> 0, kernels.py:719-722).
+ * counts (nullable): int64 (n_rows,) in-degree.
+ * err_pos (nullable unless op == DIV): device int32 slot the caller presets to
+ * INT32_MAX; receives the smallest adjacency POSITION whose divisor row holds
+ * an exact zero (kernels.py:263-268); the caller maps it to eids[pos]. */
+int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
+              const gmp_operand* lhs, const gmp_operand* rhs,
+              void* Z, int64_t ldz, int32_t d_out,
+              int64_t* arg, int64_t* counts, int32_t* err_pos,
+              const gmp_tuning* tuning, void* stream);
+
+/* ---- g-SDDMM ------------------------------------------------------------
+ * Replaces kernels.gsddmm (kernels.py:744-836), default strategy
+ * edge_parallel over COO (_gsddmm_chunked, kernels.py:732-741):
+ *   M[e] = phi(lhs, rhs)  for every edge e, in edge-id order.
+ * dot yields d_out == 1 (kernels.py:242-246). err_eid (nullable unless DIV):
+ * device int32 slot preset to INT32_MAX; receives the smallest edge id whose
+ * divisor row holds an exact zero. */
+int gmp_gsddmm(const gmp_coo* coo, int op, int dtype,
+               const gmp_operand* lhs, const gmp_operand* rhs,
+               void* M, int64_t ldm, int32_t d_out, int32_t* err_eid,
+               void* stream);
+
+/* ---- edge_softmax ---------------------------------------------------------
+ * Replaces messaging.edge_softmax (messaging.py:105-126: gspmm max, gsddmm
+ * sub, exp, gspmm sum, gsddmm div) with ONE fused per-destination pass:
+ *   alpha[e,h] = exp(s[e,h] - max_{e'->v} s[e',h]) / sum_{e'->v} exp(...)
+ * scores/alpha: (m, H) row-major keyed by edge id, leading dims lds/lda. */
+int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
+                         const void* scores, int64_t lds, int32_t H,
+                         void* alpha, int64_t lda, void* stream);
+
+/* Fused backward of edge_softmax (the composition of the four kernel
+ * backwards of messaging.py:117-121, autodiff.py:398-418):
+ *   ds[e,h] = alpha[e,h] * (g[e,h] - sum_{e'->v} alpha[e',h] g[e',h]) */
+int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
+                         const void* alpha, int64_t lda, const void* grad, int64_t ldg,
+                         int32_t H, void* ds, int64_t ldds, void* stream);
+
+/* ---- extrema gradient routing ----------------------------------------------
+ * Replaces kernels.route_extrema_grad (kernels.py:843-857): dM[arg[v,k], k] =
+ * dZ[v,k] for every cell with arg >= 0. dM (m, d) must be zero-filled by the
+ * caller (ldm). */
+int gmp_route_extrema(int64_t n_rows, int32_t d, int dtype, const int64_t* arg,
+                      const void* dZ, int64_t lddz, void* dM, int64_t ldm, void* stream);
+
+/* Fused max/min backward for copy messages: scatters dZ straight into the
+ * gradient of the copied operand without the (m, d) intermediate
+ * (autodiff.py:398-412 + _route for copy_lhs/copy_rhs). target_index: for
+ * GMP_SRC the COO src array (dX[src[arg]] += dZ), for GMP_EDGE NULL
+ * (dW[arg] = dZ). dOut must be zero-filled. Uses atomics for SRC (order of
+ * fp additions then varies; tolerance-level parity only). */
+int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* arg,
+                         const void* dZ, int64_t lddz, const int32_t* target_index,
+                         void* dOut, int64_t ldo, void* stream);
+
+/* ---- diagnostics ------------------------------------------------------------ */
+const char* gmp_last_error(void);
+const char* gmp_strerror(int status);
+/* Number of kernel launches issued by this library since load (all threads). */
+uint64_t gmp_launch_count(void);
+int gmp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMP_H_ */

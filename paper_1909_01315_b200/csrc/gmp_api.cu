@@ -1,0 +1,409 @@
+// gmp_api.cu - the extern "C" boundary of libgmp.so (declared in include/gmp.h).
+//
+// Host-side validation mirrors the reference's operand checks
+// (kernels.py:224-252, _operands_for) so that a caller gets the same class of
+// error for the same mistake; shape checks that need row counts stay in the
+// Python mirror (paper_1909_01315_b200/kernels.py), which owns the tensors.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/gmp.h"
+#include "sddmm.cuh"
+#include "softmax.cuh"
+#include "spmm_dot.cuh"
+#include "spmm_rows.cuh"
+
+namespace gmp {
+template <int OP>
+cudaError_t launch_spmm_rows(int, int, int, int, const SpmmArgs&, int64_t, cudaStream_t);
+cudaError_t launch_route_extrema(int, int64_t, int32_t, const int64_t*, const void*, int64_t, void*,
+                                 int64_t, cudaStream_t);
+cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const void*, int64_t,
+                                    const int32_t*, void*, int64_t, cudaStream_t);
+size_t schedule_workspace_bytes(int64_t n);
+cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t* order_out,
+                           void* ws, size_t ws_bytes, int64_t* n_heavy, int64_t* n_nonempty,
+                           cudaStream_t s);
+}  // namespace gmp
+
+using namespace gmp;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return GMP_OK;
+  return fail(GMP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+const char* op_name(int op) {
+  static const char* n[] = {"copy_lhs", "copy_rhs", "add", "sub", "mul", "div", "dot"};
+  return (op >= 0 && op <= 6) ? n[op] : "?";
+}
+
+bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
+
+int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int log2i(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+
+struct Opnd {
+  OperandDev dev;
+  bool present;
+};
+
+Opnd to_dev(const gmp_operand* o, int d_out) {
+  Opnd r{};
+  if (!o || !o->data) return r;
+  r.present = true;
+  r.dev.data = o->data;
+  r.dev.ld = o->ld;
+  r.dev.dim = o->dim;
+  r.dev.target = o->target;
+  r.dev.bcast = (o->dim == 1 && d_out > 1) ? 1 : 0;
+  return r;
+}
+
+// Largest vector width every full-width operand, the output and arg support.
+int pick_v(size_t F, int width, const Opnd* ops, int nops, const void* out, int64_t ldo,
+           const void* arg) {
+  const int cands[3] = {4, 2, 1};
+  for (int V : cands) {
+    if (F == 8 && V == 4) continue;
+    if (width % V) continue;
+    bool ok = true;
+    for (int i = 0; i < nops; ++i) {
+      if (!ops[i].present || ops[i].dev.bcast) continue;
+      ok &= (ops[i].dev.ld % V == 0) && aligned(ops[i].dev.data, V * F);
+    }
+    if (out) ok &= (ldo % V == 0) && aligned(out, V * F);
+    if (arg && V > 1) ok &= aligned(arg, 16);
+    if (ok) return V;
+  }
+  return 1;
+}
+
+// Validate phi's operands and derive d_out (kernels.py:224-252).
+int check_operands(int op, const gmp_operand* lhs, const gmp_operand* rhs, int32_t* d_out_expected) {
+  if (op < GMP_COPY_LHS || op > GMP_DOT) return fail(GMP_EINVAL, "unknown op %d", op);
+  const bool binary = op >= GMP_ADD;
+  const gmp_operand* used = (op == GMP_COPY_RHS) ? rhs : lhs;
+  if (!used || !used->data) return fail(GMP_EINVAL, "phi %s needs its operand", op_name(op));
+  if (used->target < GMP_SRC || used->target > GMP_EDGE)
+    return fail(GMP_EINVAL, "bad operand target %d", used->target);
+  if (used->dim < 0 || used->ld < used->dim) return fail(GMP_EINVAL, "bad operand dim/ld");
+  if (!binary) {
+    *d_out_expected = used->dim;
+    return GMP_OK;
+  }
+  if (!rhs || !rhs->data) return fail(GMP_EINVAL, "phi %s needs its rhs operand", op_name(op));
+  if (rhs->target < GMP_SRC || rhs->target > GMP_EDGE)
+    return fail(GMP_EINVAL, "bad operand target %d", rhs->target);
+  if (lhs->target == rhs->target) return fail(GMP_EINVAL, "binary op targets must differ");
+  if (rhs->dim < 0 || rhs->ld < rhs->dim) return fail(GMP_EINVAL, "bad operand dim/ld");
+  const int dl = lhs->dim, dr = rhs->dim;
+  if (op == GMP_DOT) {
+    if (dl != dr) return fail(GMP_EINVAL, "dot needs equal operand dims, got %d and %d", dl, dr);
+    *d_out_expected = 1;
+    return GMP_OK;
+  }
+  if (dl != dr && dl != 1 && dr != 1)
+    return fail(GMP_EINVAL, "operand dims %d and %d are not broadcastable", dl, dr);
+  *d_out_expected = dl > dr ? dl : dr;
+  return GMP_OK;
+}
+
+int kernel_op(int op) {
+  switch (op) {
+    case GMP_COPY_LHS:
+    case GMP_COPY_RHS: return OP_COPY;
+    case GMP_ADD: return OP_ADD;
+    case GMP_SUB: return OP_SUB;
+    case GMP_MUL: return OP_MUL;
+    case GMP_DIV: return OP_DIV;
+    default: return OP_DOT;
+  }
+}
+
+// Column-tile width: the whole row when the gathered source slice fits the
+// L2 budget, otherwise the widest slice that does (>= one 128 B line).
+int pick_tile(const gmp_tuning* tun, int d_out, int V, size_t F, int64_t n_src_rows, bool src_full,
+              int max_tw) {
+  int tw;
+  if (tun && tun->tile_cols > 0) {
+    tw = ((tun->tile_cols + V - 1) / V) * V;
+  } else {
+    tw = d_out;
+    if (src_full) {
+      const int64_t budget = (int64_t)((tun && tun->l2_budget_mb > 0) ? tun->l2_budget_mb : 64) << 20;
+      const int64_t per_col = n_src_rows * (int64_t)F;
+      const int64_t fit = per_col > 0 ? budget / per_col : d_out;
+      if (fit < d_out) {
+        const int min_cols = (int)(128 / F);
+        int64_t c = fit < min_cols ? min_cols : fit;
+        tw = (int)((c / V) * V);
+        if (tw < V) tw = V;
+      }
+    }
+  }
+  if (tw > max_tw) tw = max_tw;
+  if (tw > d_out) tw = d_out;
+  if (tw < 1) tw = 1;
+  const int ntiles = (d_out + tw - 1) / tw;
+  tw = (d_out + ntiles - 1) / ntiles;
+  tw = ((tw + V - 1) / V) * V;
+  return tw;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gmp_last_error(void) { return g_last_error.c_str(); }
+
+const char* gmp_strerror(int status) {
+  switch (status) {
+    case GMP_OK: return "ok";
+    case GMP_EINVAL: return "invalid argument";
+    case GMP_ECUDA: return "CUDA error";
+    case GMP_EUNSUPPORTED: return "unsupported configuration";
+    default: return "unknown status";
+  }
+}
+
+uint64_t gmp_launch_count(void) { return g_launches.load(); }
+
+int gmp_version(void) { return 1; }
+
+size_t gmp_schedule_workspace_size(int64_t n_rows) { return schedule_workspace_bytes(n_rows); }
+
+int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold, int32_t* order_out,
+                       void* workspace, size_t workspace_bytes, gmp_sched* sched_out,
+                       void* stream) {
+  if (!adj || !sched_out) return fail(GMP_EINVAL, "null adjacency or schedule");
+  if (adj->n_rows < 0 || adj->n_rows >= (1ll << 31)) return fail(GMP_EINVAL, "n_rows out of range");
+  if (adj->n_rows > 0 && (!order_out || !adj->indptr)) return fail(GMP_EINVAL, "null arrays");
+  if (workspace_bytes < schedule_workspace_bytes(adj->n_rows))
+    return fail(GMP_EINVAL, "workspace too small: %zu < %zu", workspace_bytes,
+                schedule_workspace_bytes(adj->n_rows));
+  int64_t nh = 0, nn = 0;
+  cudaError_t e = build_schedule(adj->n_rows, adj->indptr, heavy_threshold, order_out, workspace,
+                                 workspace_bytes, &nh, &nn, (cudaStream_t)stream);
+  g_launches += adj->n_rows > 0 ? 2 : 0;
+  if (e != cudaSuccess) return cuda_status(e, "gmp_build_schedule");
+  sched_out->order = order_out;
+  sched_out->n_heavy = nh;
+  sched_out->n_nonempty = nn;
+  sched_out->heavy_threshold = heavy_threshold;
+  return GMP_OK;
+}
+
+int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
+              const gmp_operand* lhs, const gmp_operand* rhs, void* Z, int64_t ldz, int32_t d_out,
+              int64_t* arg, int64_t* counts, int32_t* err_pos, const gmp_tuning* tuning,
+              void* stream) {
+  if (!adj) return fail(GMP_EINVAL, "null adjacency");
+  if (rho < GMP_SUM || rho > GMP_MEAN) return fail(GMP_EINVAL, "unknown reducer %d", rho);
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (adj->m < 0 || adj->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
+  if (adj->n_rows < 0 || adj->n_rows >= (1ll << 31)) return fail(GMP_EINVAL, "row count out of range");
+  int32_t want = 0;
+  int st = check_operands(op, lhs, rhs, &want);
+  if (st) return st;
+  if (d_out != want) return fail(GMP_EINVAL, "d_out %d does not match phi's output width %d", d_out, want);
+  if (ldz < d_out || (!Z && adj->n_rows > 0 && d_out > 0)) return fail(GMP_EINVAL, "bad output Z/ldz");
+  const bool ext = (rho == GMP_MAX || rho == GMP_MIN);
+  if (ext && !arg && adj->n_rows > 0 && d_out > 0) return fail(GMP_EINVAL, "max/min need the arg output");
+  if (op == GMP_DIV && !err_pos) return fail(GMP_EINVAL, "div needs the err_pos slot");
+  if (adj->n_rows == 0 || d_out == 0) return GMP_OK;
+  if (adj->m > 0 && (!adj->indices || !adj->eids)) return fail(GMP_EINVAL, "null adjacency arrays");
+  if (sched && sched->order == nullptr && sched->n_heavy > 0)
+    return fail(GMP_EINVAL, "schedule has heavy rows but no order");
+
+  const size_t F = dtype == GMP_F64 ? 8 : 4;
+  const int kop = kernel_op(op);
+  const int krho = rho == GMP_MAX ? RHO_MAX : (rho == GMP_MIN ? RHO_MIN : RHO_SUM);
+  // copy_rhs reads only its rhs: canonicalise to a copy of "lhs"
+  const gmp_operand* L = (op == GMP_COPY_RHS) ? rhs : lhs;
+  const gmp_operand* R = (kop == OP_COPY) ? nullptr : rhs;
+  Opnd ops[2] = {to_dev(L, d_out), to_dev(R, d_out)};
+  const int64_t n_heavy = sched ? sched->n_heavy : 0;
+  const int32_t* order = sched ? sched->order : nullptr;
+  const int64_t light_blocks = (adj->n_rows - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int64_t bpt = n_heavy + light_blocks;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+
+  if (kop == OP_DOT) {
+    const int dim = L->dim;
+    SpmmDotArgs a{};
+    a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
+    a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.dim = dim;
+    const int V = dim > 0 ? pick_v(F, dim, ops, 2, nullptr, 0, nullptr) : 1;
+    a.g_log2 = log2i(std::min(32, next_pow2(std::max(1, (dim + V - 1) / V))));
+    a.mean = rho == GMP_MEAN; a.lhs = ops[0].dev; a.rhs = ops[1].dev;
+    a.lhs.bcast = a.rhs.bcast = 0;
+    a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts;
+    e = launch_spmm_dot(F == 8, krho, V, a, bpt, s);
+    g_launches++;
+    return cuda_status(e, "gmp_gspmm(dot)");
+  }
+
+  const int V = pick_v(F, d_out, ops, 2, Z, ldz, ext ? arg : nullptr);
+  const bool src_full = (ops[0].dev.target == GMP_SRC && !ops[0].dev.bcast) ||
+                        (ops[1].present && ops[1].dev.target == GMP_SRC && !ops[1].dev.bcast);
+  const int max_tw = 32 * V * 2;
+  const int tw = pick_tile(tuning, d_out, V, F, adj->n_rows, src_full, max_tw);
+  const int G = std::min(32, next_pow2((tw + V - 1) / V));
+  const int P = (tw + G * V - 1) / (G * V);
+  const int ntiles = (d_out + tw - 1) / tw;
+
+  SpmmArgs a{};
+  a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
+  a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.blocks_per_tile = bpt;
+  a.d_out = d_out; a.tile_cols = tw; a.g_log2 = log2i(G); a.mean = rho == GMP_MEAN;
+  a.lhs = ops[0].dev; a.rhs = ops[1].dev;
+  a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts; a.err_pos = err_pos;
+  const int64_t grid = bpt * ntiles;
+  if (grid >= (1ll << 31)) return fail(GMP_EUNSUPPORTED, "grid too large");
+  switch (kop) {
+    case OP_COPY: e = launch_spmm_rows<OP_COPY>(F == 8, krho, V, P, a, grid, s); break;
+    case OP_ADD: e = launch_spmm_rows<OP_ADD>(F == 8, krho, V, P, a, grid, s); break;
+    case OP_SUB: e = launch_spmm_rows<OP_SUB>(F == 8, krho, V, P, a, grid, s); break;
+    case OP_MUL: e = launch_spmm_rows<OP_MUL>(F == 8, krho, V, P, a, grid, s); break;
+    default: e = launch_spmm_rows<OP_DIV>(F == 8, krho, V, P, a, grid, s); break;
+  }
+  g_launches++;
+  return cuda_status(e, "gmp_gspmm");
+}
+
+int gmp_gsddmm(const gmp_coo* coo, int op, int dtype, const gmp_operand* lhs, const gmp_operand* rhs,
+               void* M, int64_t ldm, int32_t d_out, int32_t* err_eid, void* stream) {
+  if (!coo) return fail(GMP_EINVAL, "null coo");
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (coo->m < 0 || coo->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
+  int32_t want = 0;
+  int st = check_operands(op, lhs, rhs, &want);
+  if (st) return st;
+  if (d_out != want) return fail(GMP_EINVAL, "d_out %d does not match phi's output width %d", d_out, want);
+  if (ldm < d_out || (!M && coo->m > 0 && d_out > 0)) return fail(GMP_EINVAL, "bad output M/ldm");
+  if (op == GMP_DIV && !err_eid) return fail(GMP_EINVAL, "div needs the err_eid slot");
+  if (coo->m == 0 || d_out == 0) return GMP_OK;
+  if (!coo->src || !coo->dst) return fail(GMP_EINVAL, "null coo arrays");
+  const size_t F = dtype == GMP_F64 ? 8 : 4;
+  const int kop = kernel_op(op);
+  const gmp_operand* L = (op == GMP_COPY_RHS) ? rhs : lhs;
+  const gmp_operand* R = (kop == OP_COPY) ? nullptr : rhs;
+  Opnd ops[2] = {to_dev(L, d_out), to_dev(R, d_out)};
+  SddmmArgs a{};
+  a.src = coo->src; a.dst = coo->dst; a.m = coo->m; a.d_out = d_out;
+  a.lhs = ops[0].dev; a.rhs = ops[1].dev; a.M = M; a.ldm = ldm; a.err_eid = err_eid;
+  int V, width;
+  if (kop == OP_DOT) {
+    width = L->dim;
+    a.lhs.bcast = a.rhs.bcast = 0;
+    V = width > 0 ? pick_v(F, width, ops, 2, nullptr, 0, nullptr) : 1;
+  } else {
+    width = d_out;
+    V = pick_v(F, width, ops, 2, M, ldm, nullptr);
+  }
+  a.dim = width;
+  a.g_log2 = log2i(std::min(32, next_pow2(std::max(1, (width + V - 1) / V))));
+  const int64_t warps = (coo->m + 31) / 32;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 16));
+  cudaError_t e = launch_sddmm(F == 8, kop, V, a, grid, (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_gsddmm");
+}
+
+static int softmax_common(const gmp_adj* adj, const gmp_sched* sched, int dtype, const void* s,
+                          int64_t lds, const void* g, int64_t ldg, int32_t H, void* out,
+                          int64_t ldo, bool bwd, void* stream) {
+  if (!adj) return fail(GMP_EINVAL, "null adjacency");
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (adj->m < 0 || adj->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
+  if (H < 0 || lds < H || ldo < H || (bwd && ldg < H)) return fail(GMP_EINVAL, "bad head count / ld");
+  if (adj->m == 0 || H == 0 || adj->n_rows == 0) return GMP_OK;
+  if (!s || !out || (bwd && !g) || !adj->eids || !adj->indptr) return fail(GMP_EINVAL, "null arrays");
+  const size_t F = dtype == GMP_F64 ? 8 : 4;
+  Opnd ops[2] = {};
+  ops[0].present = true; ops[0].dev.data = s; ops[0].dev.ld = lds;
+  if (bwd) { ops[1].present = true; ops[1].dev.data = g; ops[1].dev.ld = ldg; }
+  const int V = pick_v(F, H, ops, 2, out, ldo, nullptr);
+  int tw = std::min(H, 32 * V);
+  const int ntiles = (H + tw - 1) / tw;
+  tw = ((H + ntiles - 1) / ntiles + V - 1) / V * V;
+  const int G = std::min(32, next_pow2((tw + V - 1) / V));
+  const int64_t n_heavy = sched ? sched->n_heavy : 0;
+  SoftmaxArgs a{};
+  a.indptr = adj->indptr; a.eids = adj->eids; a.order = sched ? sched->order : nullptr;
+  a.n_rows = adj->n_rows; a.n_heavy = n_heavy;
+  a.blocks_per_tile = n_heavy + (adj->n_rows - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
+  a.H = H; a.tile_cols = tw; a.g_log2 = log2i(G);
+  a.s = s; a.lds = lds; a.g = g; a.ldg = ldg; a.out = out; a.ldo = ldo;
+  cudaError_t e = launch_edge_softmax(F == 8, V, bwd, a, a.blocks_per_tile * ntiles,
+                                      (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, bwd ? "gmp_edge_softmax_bwd" : "gmp_edge_softmax_fwd");
+}
+
+int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
+                         const void* scores, int64_t lds, int32_t H, void* alpha, int64_t lda,
+                         void* stream) {
+  return softmax_common(in_adj, sched, dtype, scores, lds, nullptr, 0, H, alpha, lda, false, stream);
+}
+
+int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
+                         const void* alpha, int64_t lda, const void* grad, int64_t ldg, int32_t H,
+                         void* ds, int64_t ldds, void* stream) {
+  return softmax_common(in_adj, sched, dtype, alpha, lda, grad, ldg, H, ds, ldds, true, stream);
+}
+
+int gmp_route_extrema(int64_t n_rows, int32_t d, int dtype, const int64_t* arg, const void* dZ,
+                      int64_t lddz, void* dM, int64_t ldm, void* stream) {
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (n_rows < 0 || d < 0 || lddz < d || ldm < d) return fail(GMP_EINVAL, "bad sizes");
+  if (n_rows == 0 || d == 0) return GMP_OK;
+  if (!arg || !dZ || !dM) return fail(GMP_EINVAL, "null arrays");
+  cudaError_t e = launch_route_extrema(dtype == GMP_F64, n_rows, d, arg, dZ, lddz, dM, ldm,
+                                       (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_route_extrema");
+}
+
+int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* arg, const void* dZ,
+                         int64_t lddz, const int32_t* target_index, void* dOut, int64_t ldo,
+                         void* stream) {
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (n_rows < 0 || d < 0 || lddz < d || ldo < d) return fail(GMP_EINVAL, "bad sizes");
+  if (n_rows == 0 || d == 0) return GMP_OK;
+  if (!arg || !dZ || !dOut) return fail(GMP_EINVAL, "null arrays");
+  cudaError_t e = launch_extrema_bwd_copy(dtype == GMP_F64, n_rows, d, arg, dZ, lddz, target_index,
+                                          dOut, ldo, (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_extrema_bwd_copy");
+}
+
+}  // extern "C"

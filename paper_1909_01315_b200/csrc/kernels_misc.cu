@@ -1,0 +1,206 @@
+// kernels_misc.cu - launchers for the dot / SDDMM / softmax kernels, the
+// extrema gradient kernels and the degree-binned schedule builder.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "sddmm.cuh"
+#include "softmax.cuh"
+#include "spmm_dot.cuh"
+
+namespace gmp {
+
+cudaError_t launch_spmm_dot(int f64, int rho, int V, const SpmmDotArgs& a, int64_t grid,
+                            cudaStream_t s) {
+#define GMP_DOT(T, R, VV) spmm_dot_kernel<T, R, VV><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a)
+#define GMP_DOT_V(T, R)            \
+  do {                             \
+    if (V == 4 && sizeof(T) == 4)  \
+      GMP_DOT(float, R, 4);        \
+    else if (V == 2)               \
+      GMP_DOT(T, R, 2);            \
+    else                           \
+      GMP_DOT(T, R, 1);            \
+  } while (0)
+  if (f64) {
+    if (rho == RHO_SUM) GMP_DOT_V(double, RHO_SUM);
+    else if (rho == RHO_MAX) GMP_DOT_V(double, RHO_MAX);
+    else GMP_DOT_V(double, RHO_MIN);
+  } else {
+    if (rho == RHO_SUM) GMP_DOT_V(float, RHO_SUM);
+    else if (rho == RHO_MAX) GMP_DOT_V(float, RHO_MAX);
+    else GMP_DOT_V(float, RHO_MIN);
+  }
+#undef GMP_DOT_V
+#undef GMP_DOT
+  return cudaGetLastError();
+}
+
+template <typename T, int OP>
+static void sddmm_v(int V, const SddmmArgs& a, int64_t grid, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {
+    if (V == 4) { sddmm_kernel<T, OP, 4><<<(unsigned)grid, 256, 0, s>>>(a); return; }
+  }
+  if (V == 2) { sddmm_kernel<T, OP, 2><<<(unsigned)grid, 256, 0, s>>>(a); return; }
+  sddmm_kernel<T, OP, 1><<<(unsigned)grid, 256, 0, s>>>(a);
+}
+
+template <typename T>
+static void sddmm_op(int op, int V, const SddmmArgs& a, int64_t grid, cudaStream_t s) {
+  switch (op) {
+    case OP_COPY: sddmm_v<T, OP_COPY>(V, a, grid, s); break;
+    case OP_ADD: sddmm_v<T, OP_ADD>(V, a, grid, s); break;
+    case OP_SUB: sddmm_v<T, OP_SUB>(V, a, grid, s); break;
+    case OP_MUL: sddmm_v<T, OP_MUL>(V, a, grid, s); break;
+    case OP_DIV: sddmm_v<T, OP_DIV>(V, a, grid, s); break;
+    default: sddmm_v<T, OP_DOT>(V, a, grid, s); break;
+  }
+}
+
+cudaError_t launch_sddmm(int f64, int op, int V, const SddmmArgs& a, int64_t grid, cudaStream_t s) {
+  if (f64) sddmm_op<double>(op, V, a, grid, s);
+  else sddmm_op<float>(op, V, a, grid, s);
+  return cudaGetLastError();
+}
+
+template <typename T, bool BWD>
+static void softmax_v(int V, const SoftmaxArgs& a, int64_t grid, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {
+    if (V == 4) { edge_softmax_kernel<T, 4, BWD><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a); return; }
+  }
+  if (V == 2) { edge_softmax_kernel<T, 2, BWD><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a); return; }
+  edge_softmax_kernel<T, 1, BWD><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
+}
+
+cudaError_t launch_edge_softmax(int f64, int V, bool bwd, const SoftmaxArgs& a, int64_t grid,
+                                cudaStream_t s) {
+  if (f64) {
+    if (bwd) softmax_v<double, true>(V, a, grid, s);
+    else softmax_v<double, false>(V, a, grid, s);
+  } else {
+    if (bwd) softmax_v<float, true>(V, a, grid, s);
+    else softmax_v<float, false>(V, a, grid, s);
+  }
+  return cudaGetLastError();
+}
+
+// ---- extrema gradient routing (kernels.py:843-857) --------------------------
+
+template <typename T>
+__global__ void route_extrema_kernel(int64_t n, int32_t d, const int64_t* __restrict__ arg,
+                                     const T* __restrict__ dZ, int64_t lddz, T* dM, int64_t ldm) {
+  const int64_t total = n * (int64_t)d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / d;
+    const int k = (int)(i - v * d);
+    const int64_t e = arg[i];
+    if (e >= 0) dM[e * ldm + k] = dZ[v * lddz + k];
+  }
+}
+
+template <typename T>
+__global__ void extrema_bwd_copy_kernel(int64_t n, int32_t d, const int64_t* __restrict__ arg,
+                                        const T* __restrict__ dZ, int64_t lddz,
+                                        const int32_t* __restrict__ tindex, T* dOut, int64_t ldo) {
+  const int64_t total = n * (int64_t)d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / d;
+    const int k = (int)(i - v * d);
+    const int64_t e = arg[i];
+    if (e < 0) continue;
+    const T g = dZ[v * lddz + k];
+    if (tindex) atomicAdd(dOut + (int64_t)tindex[e] * ldo + k, g);
+    else dOut[e * ldo + k] = g;  // one winner per (edge, column)
+  }
+}
+
+cudaError_t launch_route_extrema(int f64, int64_t n, int32_t d, const int64_t* arg, const void* dZ,
+                                 int64_t lddz, void* dM, int64_t ldm, cudaStream_t s) {
+  const int64_t total = n * (int64_t)d;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  if (total == 0) return cudaSuccess;
+  if (f64) route_extrema_kernel<double><<<grid, 256, 0, s>>>(n, d, arg, (const double*)dZ, lddz, (double*)dM, ldm);
+  else route_extrema_kernel<float><<<grid, 256, 0, s>>>(n, d, arg, (const float*)dZ, lddz, (float*)dM, ldm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_extrema_bwd_copy(int f64, int64_t n, int32_t d, const int64_t* arg,
+                                    const void* dZ, int64_t lddz, const int32_t* tindex,
+                                    void* dOut, int64_t ldo, cudaStream_t s) {
+  const int64_t total = n * (int64_t)d;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  if (total == 0) return cudaSuccess;
+  if (f64) extrema_bwd_copy_kernel<double><<<grid, 256, 0, s>>>(n, d, arg, (const double*)dZ, lddz, tindex, (double*)dOut, ldo);
+  else extrema_bwd_copy_kernel<float><<<grid, 256, 0, s>>>(n, d, arg, (const float*)dZ, lddz, tindex, (float*)dOut, ldo);
+  return cudaGetLastError();
+}
+
+// ---- degree-binned schedule ---------------------------------------------------
+
+__global__ void degree_kernel(int64_t n, const int64_t* __restrict__ indptr, int32_t* deg,
+                              int32_t* rows, int32_t thr, unsigned long long* counters) {
+  unsigned long long heavy = 0, nonempty = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t dg = indptr[r + 1] - indptr[r];
+    deg[r] = (int32_t)dg;
+    rows[r] = (int32_t)r;
+    heavy += dg > thr;
+    nonempty += dg > 0;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    heavy += __shfl_xor_sync(kFull, heavy, off);
+    nonempty += __shfl_xor_sync(kFull, nonempty, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (heavy) atomicAdd(counters, heavy);
+    if (nonempty) atomicAdd(counters + 1, nonempty);
+  }
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t schedule_cub_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending((void*)nullptr, bytes, (const int32_t*)nullptr,
+                                            (int32_t*)nullptr, (const int32_t*)nullptr,
+                                            (int32_t*)nullptr, (int)n);
+  return bytes;
+}
+
+size_t schedule_workspace_bytes(int64_t n) {
+  return align256(16) + 3 * align256((size_t)n * 4) + align256(schedule_cub_bytes(n));
+}
+
+cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t* order_out,
+                           void* ws, size_t ws_bytes, int64_t* n_heavy, int64_t* n_nonempty,
+                           cudaStream_t s) {
+  char* p = static_cast<char*>(ws);
+  auto* counters = reinterpret_cast<unsigned long long*>(p);
+  p += align256(16);
+  auto* deg = reinterpret_cast<int32_t*>(p);
+  p += align256((size_t)n * 4);
+  auto* deg_sorted = reinterpret_cast<int32_t*>(p);
+  p += align256((size_t)n * 4);
+  auto* rows = reinterpret_cast<int32_t*>(p);
+  p += align256((size_t)n * 4);
+  size_t cub_bytes = ws_bytes - (size_t)(p - static_cast<char*>(ws));
+  cudaError_t err = cudaMemsetAsync(counters, 0, 16, s);
+  if (err != cudaSuccess) return err;
+  if (n > 0) {
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    degree_kernel<<<grid, 256, 0, s>>>(n, indptr, deg, rows, thr, counters);
+    err = cub::DeviceRadixSort::SortPairsDescending(p, cub_bytes, deg, deg_sorted, rows, order_out,
+                                                    (int)n, 0, 32, s);
+    if (err != cudaSuccess) return err;
+  }
+  unsigned long long host[2] = {0, 0};
+  err = cudaMemcpyAsync(host, counters, 16, cudaMemcpyDeviceToHost, s);
+  if (err != cudaSuccess) return err;
+  err = cudaStreamSynchronize(s);
+  *n_heavy = (int64_t)host[0];
+  *n_nonempty = (int64_t)host[1];
+  return err;
+}
+
+}  // namespace gmp

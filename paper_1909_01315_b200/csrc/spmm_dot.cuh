@@ -1,0 +1,123 @@
+// spmm_dot.cuh - g-SpMM with a dot-product message (d_out == 1).
+//
+// Replaces gspmm for phi = dot(a, b) (kernels.py:290-293: the message is the
+// row sum of a*b, one column). Same row schedule as spmm_rows.cuh; inside a
+// warp, G lanes cooperate on one edge's dot (fp64 partials, xor-shuffle tree),
+// E = 32 / G edges run side by side, then rho reduces across edge slots.
+#pragma once
+
+#include "gmp_common.cuh"
+#include "spmm_rows.cuh"
+
+namespace gmp {
+
+struct SpmmDotArgs {
+  const int64_t* indptr;
+  const int32_t* indices;
+  const int32_t* eids;
+  const int32_t* order;
+  int64_t n_rows;
+  int64_t n_heavy;
+  int32_t dim;     // operand width
+  int32_t g_log2;  // lanes per edge
+  int32_t mean;
+  OperandDev lhs, rhs;
+  void* Z;
+  int64_t ldz;
+  int64_t* arg;
+  int64_t* counts;
+};
+
+template <typename T, int V>
+__device__ __forceinline__ double dot_partial(const OperandDev& a, const OperandDev& b, int64_t row,
+                                              int32_t nbr, int32_t eid, int gl, int G, int dim) {
+  const int64_t ra = a.target == T_SRC ? nbr : (a.target == T_DST ? row : eid);
+  const int64_t rb = b.target == T_SRC ? nbr : (b.target == T_DST ? row : eid);
+  const T* pa = static_cast<const T*>(a.data) + ra * a.ld;
+  const T* pb = static_cast<const T*>(b.data) + rb * b.ld;
+  double s = 0.0;
+  for (int c = gl * V; c < dim; c += G * V) {
+    T xa[V], xb[V];
+    load_vec<T, V>(pa + c, xa);
+    load_vec<T, V>(pb + c, xb);
+#pragma unroll
+    for (int k = 0; k < V; ++k) s += (double)xa[k] * (double)xb[k];
+  }
+  return s;
+}
+
+template <typename T, int RHO, int V>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) spmm_dot_kernel(const SpmmDotArgs a) {
+  __shared__ double s_acc[kWarpsPerCta];
+  __shared__ int32_t s_arg[kWarpsPerCta];
+  const int64_t local = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = 1 << a.g_log2, E = 32 >> a.g_log2;
+  const int slot = lane >> a.g_log2, gl = lane & (G - 1);
+  const bool heavy = local < a.n_heavy;
+  int64_t row;
+  if (heavy) {
+    row = a.order[local];
+  } else {
+    const int64_t r = a.n_heavy + (local - a.n_heavy) * kWarpsPerCta + warp;
+    if (r >= a.n_rows) return;
+    row = a.order ? (int64_t)a.order[r] : r;
+  }
+  const int64_t pb = a.indptr[row], pe = a.indptr[row + 1], deg = pe - pb;
+  double acc = (RHO == RHO_SUM) ? 0.0 : ext_init<RHO>();
+  int32_t arg = 0x7fffffff;
+  const int64_t first = heavy ? (int64_t)warp * 32 : 0;
+  const int64_t stride = heavy ? 32 * kWarpsPerCta : 32;
+  for (int64_t base = pb + first; base < pe; base += stride) {
+    const int cnt = batch_count(pe - base);
+    int nb = 0, eb = 0;
+    if (lane < cnt) {
+      nb = __ldg(a.indices + base + lane);
+      eb = __ldg(a.eids + base + lane);
+    }
+    for (int t = 0; t < cnt; t += E) {
+      const int j = t + slot;
+      const int32_t uu = __shfl_sync(kFull, nb, j & 31);
+      const int32_t ee = __shfl_sync(kFull, eb, j & 31);
+      double s = 0.0;
+      if (j < cnt) s = dot_partial<T, V>(a.lhs, a.rhs, row, uu, ee, gl, G, a.dim);
+      for (int off = 1; off < G; off <<= 1) s += shfl_xor_d(s, off);
+      if (j < cnt) {
+        if constexpr (RHO == RHO_SUM) acc += s;
+        else ext_update<RHO>(acc, arg, s, ee);
+      }
+    }
+  }
+  for (int off = G; off < 32; off <<= 1) {
+    const double o = shfl_xor_d(acc, off);
+    if constexpr (RHO == RHO_SUM) acc += o;
+    else ext_update<RHO>(acc, arg, o, __shfl_xor_sync(kFull, arg, off));
+  }
+  if (heavy) {
+    if (lane == 0) { s_acc[warp] = acc; s_arg[warp] = arg; }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    acc = s_acc[0]; arg = s_arg[0];
+    for (int w = 1; w < kWarpsPerCta; ++w) {
+      if constexpr (RHO == RHO_SUM) acc += s_acc[w];
+      else ext_update<RHO>(acc, arg, s_acc[w], s_arg[w]);
+    }
+  } else if (lane != 0) {
+    return;
+  }
+  T* z = static_cast<T*>(a.Z) + row * a.ldz;
+  if (a.counts) a.counts[row] = deg;
+  if constexpr (RHO == RHO_SUM) {
+    double v = acc;
+    if (a.mean && deg > 0) v = v / (double)deg;
+    *z = (T)v;
+  } else {
+    *z = deg > 0 ? (T)acc : T(0);
+    a.arg[row] = deg > 0 ? arg : -1;
+  }
+}
+
+cudaError_t launch_spmm_dot(int dtype_is_f64, int rho, int V, const SpmmDotArgs& a, int64_t grid,
+                            cudaStream_t s);
+
+}  // namespace gmp

@@ -1,0 +1,540 @@
+"""g-SpMM / g-SDDMM on B200: the reference's kernel-engine API over libgmp.so.
+
+Drop-in for /root/reference/pkg/src/graphmp/kernels.py. Same names, same
+argument meaning, same validation errors (ValueError texts of
+kernels.py:86-97,217-251,692-701,748-759; ZeroDivisionError naming the edge,
+kernels.py:263-268), same return shapes:
+
+  gspmm(g, phi, rho, X, Y, W, ...) -> (Z, aux)   aux: None | counts | ArgExtrema
+  gsddmm(g, phi, X, Y, W, ...)     -> M
+
+Differences that are the point of the port:
+  * every call is one launch of a hand-written sm_100a kernel through the
+    C-ABI (include/gmp.h); there is no CPU path - a graph or operand that is
+    not on a CUDA device raises;
+  * results are torch tensors on the graph's device. Operand dtype is kept:
+    float32 operands run the fp32 kernels, float64 (e.g. numpy defaults) the
+    fp64 ones; mixed operands are promoted to float64 (the reference coerces
+    everything to float64, kernels.py:216);
+  * `strategy` / `fmt` keep their names and legality tables
+    (kernels.py:47-65) and select a GPU schedule; every schedule returns
+    identical results (deterministic, no float atomics). num_workers and
+    block_edges are CPU-thread knobs and are accepted but unused.
+"""
+
+import ctypes
+import threading
+from contextlib import contextmanager
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, accounting
+from .graph import HEAVY_ROW_THRESHOLD
+
+BLOCK_EDGES = 2048  # reference chunk size (kernels.py:39); device kernels need no host chunking
+
+OPS = ("copy_lhs", "copy_rhs", "add", "sub", "mul", "div", "dot")
+TARGETS = ("src", "dst", "edge")
+REDUCERS = ("sum", "max", "min", "mean")
+
+GSPMM_STRATEGIES = ("node_parallel", "edge_parallel", "edge_parallel_atomic",
+                    "feature_parallel", "serial_reference")
+GSDDMM_STRATEGIES = ("node_parallel", "edge_parallel", "feature_parallel",
+                     "serial_reference")
+_GSPMM_FORMATS = {
+    "node_parallel": ("csc",),
+    "edge_parallel": ("csc",),
+    "edge_parallel_atomic": ("coo", "csr", "csc"),
+    "feature_parallel": ("csc",),
+    "serial_reference": ("coo",),
+}
+_GSDDMM_FORMATS = {
+    "node_parallel": ("csr", "csc"),
+    "edge_parallel": ("coo", "csr", "csc"),
+    "feature_parallel": ("coo", "csr", "csc"),
+    "serial_reference": ("coo",),
+}
+_INT32_MAX = 2 ** 31 - 1
+
+
+# ----------------------------------------------------------------------------
+# message function descriptors (kernels.py:72-144)
+
+
+@dataclass(frozen=True)
+class MessageFunc:
+    """op plus the operand target(s) it reads; see kernels.py:72-104."""
+    op: str
+    lhs_target: str = None
+    rhs_target: str = None
+
+    def __post_init__(self):
+        if self.op not in OPS:
+            raise ValueError("unknown op %r" % (self.op,))
+        if self.op == "copy_lhs":
+            if self.lhs_target not in TARGETS or self.rhs_target is not None:
+                raise ValueError("copy_lhs takes exactly one lhs target")
+        elif self.op == "copy_rhs":
+            if self.rhs_target not in TARGETS or self.lhs_target is not None:
+                raise ValueError("copy_rhs takes exactly one rhs target")
+        else:
+            if self.lhs_target not in TARGETS or self.rhs_target not in TARGETS:
+                raise ValueError("%s takes lhs and rhs targets" % self.op)
+            if self.lhs_target == self.rhs_target:
+                raise ValueError("binary op targets must differ")
+
+    @property
+    def targets(self):
+        return tuple(t for t in (self.lhs_target, self.rhs_target) if t is not None)
+
+    def describe(self):
+        return "%s(%s)" % (self.op, ",".join(self.targets))
+
+
+def copy(target):
+    return MessageFunc("copy_lhs", lhs_target=target)
+
+
+def copy_rhs(target):
+    return MessageFunc("copy_rhs", rhs_target=target)
+
+
+def add(lhs, rhs):
+    return MessageFunc("add", lhs, rhs)
+
+
+def sub(lhs, rhs):
+    return MessageFunc("sub", lhs, rhs)
+
+
+def mul(lhs, rhs):
+    return MessageFunc("mul", lhs, rhs)
+
+
+def div(lhs, rhs):
+    return MessageFunc("div", lhs, rhs)
+
+
+def dot(lhs, rhs):
+    return MessageFunc("dot", lhs, rhs)
+
+
+def builtin_message_funcs():
+    """The 30 built-in phis in the reference's canonical order (kernels.py:136-144)."""
+    out = [copy(t) for t in TARGETS]
+    pairs = (("src", "dst"), ("dst", "src"), ("src", "edge"), ("edge", "src"),
+             ("dst", "edge"), ("edge", "dst"))
+    for op in ("add", "sub", "mul", "div"):
+        out.extend(MessageFunc(op, a, b) for a, b in pairs)
+    out.extend(dot(a, b) for a, b in (("src", "dst"), ("src", "edge"), ("dst", "edge")))
+    return out
+
+
+@dataclass
+class ArgExtrema:
+    """Winning edge id per max/min cell: int64 device tensor, -1 on empty rows."""
+    arg_edge: torch.Tensor
+
+    @property
+    def empty_rows(self):
+        return self.arg_edge[:, 0] < 0
+
+
+# ----------------------------------------------------------------------------
+# configuration (kernels.py:161-206)
+
+_config = threading.local()
+
+
+@contextmanager
+def force_strategy(name):
+    prev = getattr(_config, "strategy", None)
+    _config.strategy = name
+    try:
+        yield
+    finally:
+        _config.strategy = prev
+
+
+@contextmanager
+def default_workers(n):
+    prev = getattr(_config, "workers", 1)
+    _config.workers = int(n)
+    try:
+        yield
+    finally:
+        _config.workers = prev
+
+
+@contextmanager
+def tuning(tile_cols=None, l2_budget_mb=None):
+    """Thread-local override of the row kernels' column tile / L2 budget."""
+    prev = getattr(_config, "tuning", None)
+    _config.tuning = (tile_cols or 0, l2_budget_mb or 0)
+    try:
+        yield
+    finally:
+        _config.tuning = prev
+
+
+def select_format(kernel, direction="forward"):
+    """gspmm walks the in-adjacency (csc; its backward the reverse graph's csc
+    == the forward csr); gsddmm walks the edge list (coo). kernels.py:193-206."""
+    if kernel == "gspmm":
+        return "csc"
+    if kernel == "gsddmm":
+        return "coo"
+    raise ValueError("unknown kernel %r" % (kernel,))
+
+
+# ----------------------------------------------------------------------------
+# operand plumbing
+
+
+def _require_cuda(g):
+    if g.device.type != "cuda":
+        raise RuntimeError(
+            "paper_1909_01315_b200 kernels run only on a CUDA device (graph is on %s); "
+            "there is no CPU fallback" % g.device)
+
+
+def _to_tensor(name, M, device):
+    if isinstance(M, torch.Tensor):
+        t = M
+        if not (t.dtype == torch.float32 or t.dtype == torch.float64):
+            t = t.to(torch.float32 if t.is_floating_point() else torch.float64)
+    else:
+        a = np.asarray(M)
+        if a.dtype != np.float32:
+            a = a.astype(np.float64)
+        t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.dim() != 2:
+        raise ValueError("%s must be a 2-D matrix, got ndim=%d" % (name, t.dim()))
+    if t.device != device:
+        t = t.to(device)
+    if t.shape[1] > 1 and t.stride(1) != 1:
+        t = t.contiguous()
+    return t
+
+
+def _as_matrix(name, M, rows, device):
+    if M is None:
+        return None
+    t = _to_tensor(name, M, device)
+    if t.shape[0] != rows:
+        raise ValueError("%s has %d rows, expected %d" % (name, t.shape[0], rows))
+    return t
+
+
+def _operands_for(g, phi, X, Y, W):
+    """Validate presence and shapes (kernels.py:224-252); return X, Y, W, d_out."""
+    needed = set(phi.targets)
+    if "src" in needed and X is None:
+        raise ValueError("phi %s needs X (source rows)" % phi.describe())
+    if "dst" in needed and Y is None:
+        raise ValueError("phi %s needs Y (destination rows)" % phi.describe())
+    if "edge" in needed and W is None:
+        raise ValueError("phi %s needs W (edge rows)" % phi.describe())
+    dev = g.device
+    X = _as_matrix("X", X, g.num_nodes, dev) if "src" in needed else None
+    Y = _as_matrix("Y", Y, g.num_nodes, dev) if "dst" in needed else None
+    W = _as_matrix("W", W, g.num_edges, dev) if "edge" in needed else None
+    mats = {"src": X, "dst": Y, "edge": W}
+    if any(m is not None and m.dtype == torch.float64 for m in mats.values()):
+        mats = {k: (None if m is None else m.to(torch.float64)) for k, m in mats.items()}
+    X, Y, W = mats["src"], mats["dst"], mats["edge"]
+
+    def dim(t):
+        return mats[t].shape[1]
+
+    if phi.op in ("copy_lhs", "copy_rhs"):
+        d_out = dim(phi.targets[0])
+    elif phi.op == "dot":
+        dl, dr = dim(phi.lhs_target), dim(phi.rhs_target)
+        if dl != dr:
+            raise ValueError("dot needs equal operand dims, got %d and %d" % (dl, dr))
+        d_out = 1
+    else:
+        dl, dr = dim(phi.lhs_target), dim(phi.rhs_target)
+        if dl != dr and 1 not in (dl, dr):
+            raise ValueError("operand dims %d and %d are not broadcastable" % (dl, dr))
+        d_out = max(dl, dr)
+    return X, Y, W, d_out
+
+
+def _dtype_code(t):
+    return _lib.GMP_F64 if t.dtype == torch.float64 else _lib.GMP_F32
+
+
+def _ld(t):
+    return max(int(t.stride(0)), int(t.shape[1])) if t.shape[0] > 1 else int(t.shape[1])
+
+
+_dummy = {}
+
+
+def _data_ptr(t):
+    """Device address of t; empty tensors get a valid dummy address (never read)."""
+    if t.numel():
+        return t.data_ptr()
+    d = _dummy.get(t.device)
+    if d is None:
+        d = _dummy.setdefault(t.device, torch.zeros(4, dtype=torch.float64, device=t.device))
+    return d.data_ptr()
+
+
+def _operand(t, target):
+    if t is None:
+        return None
+    return _lib.GmpOperand(_data_ptr(t), _ld(t), int(t.shape[1]), _lib.TARGETS[target])
+
+
+def _phi_operands(phi, X, Y, W):
+    mats = {"src": X, "dst": Y, "edge": W}
+    lhs = _operand(mats[phi.lhs_target], phi.lhs_target) if phi.lhs_target else None
+    rhs = _operand(mats[phi.rhs_target], phi.rhs_target) if phi.rhs_target else None
+    return lhs, rhs
+
+
+def _ptr(obj):
+    return None if obj is None else ctypes.byref(obj)
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _adj_struct(adj):
+    s = adj._extra.get("struct")
+    if s is None:
+        s = _lib.GmpAdj(adj.num_groups, adj.indices.numel(), adj.indptr.data_ptr(),
+                        adj.indices.data_ptr(), adj.edge_ids.data_ptr())
+        adj._extra["struct"] = s
+    return s
+
+
+class _Schedule:
+    __slots__ = ("struct", "order", "n_heavy", "n_nonempty")
+
+
+def _build_schedule(adj):
+    """Degree-sorted row order + heavy-row count (gmp_build_schedule)."""
+    lib = _lib.load()
+    n = adj.num_groups
+    dev = adj.indptr.device
+    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    ws_bytes = int(lib.gmp_schedule_workspace_size(n))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    sched = _lib.GmpSched()
+    _lib.check(lib.gmp_build_schedule(ctypes.byref(_adj_struct(adj)), HEAVY_ROW_THRESHOLD,
+                                      order.data_ptr(), ws.data_ptr(), ws_bytes,
+                                      ctypes.byref(sched), _stream(dev)), "gmp_build_schedule")
+    out = _Schedule()
+    out.struct, out.order = sched, order
+    out.n_heavy, out.n_nonempty = int(sched.n_heavy), int(sched.n_nonempty)
+    return out
+
+
+def _tuning_struct(strategy):
+    tc, l2 = getattr(_config, "tuning", None) or (0, 0)
+    if strategy == "feature_parallel" and not tc:
+        tc = 32  # the reference's column split, one 128 B line per row slice
+    if not tc and not l2:
+        return None
+    return _lib.GmpTuning(int(tc), 0, int(l2))
+
+
+def _err_slot(device):
+    return torch.full((1,), _INT32_MAX, dtype=torch.int32, device=device)
+
+
+def _raise_div_zero(eid):
+    raise ZeroDivisionError("division by zero in edge message at edge id %d" % int(eid))
+
+
+# ----------------------------------------------------------------------------
+# g-SpMM (kernels.py:685-725)
+
+
+def _resolve_strategy(kind, strategy, fmt):
+    if kind == "gspmm":
+        strategy = strategy or getattr(_config, "strategy", None) or "node_parallel"
+        if strategy not in GSPMM_STRATEGIES:
+            raise ValueError("unknown gspmm strategy %r" % (strategy,))
+        allowed = _GSPMM_FORMATS[strategy]
+    else:
+        if strategy == "edge_parallel_atomic":
+            raise ValueError("gsddmm writes disjoint rows; it has no atomic variant")
+        forced = getattr(_config, "strategy", None)
+        if forced == "edge_parallel_atomic":
+            forced = "edge_parallel"
+        strategy = strategy or forced or "edge_parallel"
+        if strategy not in GSDDMM_STRATEGIES:
+            raise ValueError("unknown gsddmm strategy %r" % (strategy,))
+        allowed = _GSDDMM_FORMATS[strategy]
+    fmt = fmt or allowed[0]
+    if fmt not in allowed:
+        raise ValueError("%s strategy %s cannot run on format %s" % (kind, strategy, fmt))
+    return strategy, fmt
+
+
+def gspmm(g, phi, rho, X=None, Y=None, W=None, strategy=None, num_workers=None,
+          fmt=None, block_edges=None):
+    """Reduce per-edge messages into one row per destination: (Z, aux)."""
+    if rho not in REDUCERS:
+        raise ValueError("unknown reducer %r" % (rho,))
+    X, Y, W, d_out = _operands_for(g, phi, X, Y, W)
+    strategy, fmt = _resolve_strategy("gspmm", strategy, fmt)
+    accounting.log_dispatch("gspmm", g.uid, phi.describe(), rho, strategy, g.num_nodes, d_out)
+    _require_cuda(g)
+    return _gspmm_launch(g, phi, rho, X, Y, W, d_out, _tuning_struct(strategy))
+
+
+def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None):
+    lib = _lib.load()
+    dev = g.device
+    n = g.num_nodes
+    ref = next(t for t in (X, Y, W) if t is not None)
+    Z = out if out is not None else accounting.register(
+        torch.empty((n, d_out), dtype=ref.dtype, device=dev))
+    arg = None
+    if rho in ("max", "min"):
+        arg = accounting.register(torch.empty((n, d_out), dtype=torch.int64, device=dev))
+    adj = g.to_csc()
+    err = _err_slot(dev) if phi.op == "div" else None
+    lhs, rhs = _phi_operands(phi, X, Y, W)
+    sched = adj.schedule() if n > 0 else None
+    st = lib.gmp_gspmm(ctypes.byref(_adj_struct(adj)),
+                       ctypes.byref(sched.struct) if sched is not None else None,
+                       _lib.OPS[phi.op], _lib.RHOS[rho], _dtype_code(ref),
+                       _ptr(lhs), _ptr(rhs), _data_ptr(Z),
+                       _ld(Z) if Z.dim() == 2 and Z.shape[0] else max(d_out, 1), d_out,
+                       _data_ptr(arg) if arg is not None else None,
+                       None, err.data_ptr() if err is not None else None,
+                       _ptr(tune), _stream(dev))
+    _lib.check(st, "gmp_gspmm")
+    if err is not None:
+        pos = int(err.item())
+        if pos != _INT32_MAX:
+            _raise_div_zero(adj.edge_ids[pos].item())
+    if rho == "mean":
+        return Z, adj.degrees().clone()
+    if arg is not None:
+        return Z, ArgExtrema(arg)
+    return Z, None
+
+
+# ----------------------------------------------------------------------------
+# g-SDDMM (kernels.py:744-836)
+
+
+def gsddmm(g, phi, X=None, Y=None, W=None, strategy=None, num_workers=None, fmt=None,
+           block_edges=None):
+    """Per-edge messages: one output row per edge, in edge-id order."""
+    X, Y, W, d_out = _operands_for(g, phi, X, Y, W)
+    strategy, fmt = _resolve_strategy("gsddmm", strategy, fmt)
+    m = g.num_edges
+    accounting.log_dispatch("gsddmm", g.uid, phi.describe(), "-", strategy, m, d_out)
+    _require_cuda(g)
+    return _gsddmm_launch(g, phi, X, Y, W, d_out)
+
+
+def _gsddmm_launch(g, phi, X, Y, W, d_out, out=None):
+    lib = _lib.load()
+    dev = g.device
+    m = g.num_edges
+    ref = next(t for t in (X, Y, W) if t is not None)
+    M = out if out is not None else accounting.register(
+        torch.empty((m, d_out), dtype=ref.dtype, device=dev))
+    err = _err_slot(dev) if phi.op == "div" else None
+    lhs, rhs = _phi_operands(phi, X, Y, W)
+    coo = _lib.GmpCoo(g.num_nodes, m, g.src.data_ptr(), g.dst.data_ptr())
+    st = lib.gmp_gsddmm(ctypes.byref(coo), _lib.OPS[phi.op], _dtype_code(ref), _ptr(lhs),
+                        _ptr(rhs), _data_ptr(M),
+                        _ld(M) if M.shape[0] else max(d_out, 1), d_out,
+                        err.data_ptr() if err is not None else None, _stream(dev))
+    _lib.check(st, "gmp_gsddmm")
+    if err is not None:
+        e = int(err.item())
+        if e != _INT32_MAX:
+            _raise_div_zero(e)
+    return M
+
+
+# ----------------------------------------------------------------------------
+# extrema gradient routing (kernels.py:843-857)
+
+
+def route_extrema_grad(g, aux, dZ, d_out):
+    """dM[arg[v,k], k] = dZ[v,k]: the (m, d_out) edge-keyed upstream of a max/min."""
+    accounting.log_dispatch("gsddmm", g.uid, "argext_route", "-", "edge_parallel",
+                            g.num_edges, d_out)
+    _require_cuda(g)
+    arg = aux.arg_edge
+    dZ = _to_tensor("dZ", dZ, g.device)
+    dM = accounting.register(torch.zeros((g.num_edges, d_out), dtype=dZ.dtype, device=g.device))
+    if dM.numel():
+        _lib.check(_lib.load().gmp_route_extrema(
+            arg.shape[0], d_out, _dtype_code(dZ), arg.contiguous().data_ptr(), dZ.data_ptr(),
+            _ld(dZ), dM.data_ptr(), d_out, _stream(g.device)), "gmp_route_extrema")
+    return dM
+
+
+def extrema_backward_copy(g, aux, dZ, target, rows):
+    """Fused max/min backward of a copy message: scatter dZ straight into the
+    copied operand's gradient (no (m, d) buffer). target 'src' -> dX (rows n),
+    'edge' -> dW (rows m)."""
+    _require_cuda(g)
+    arg = aux.arg_edge.contiguous()
+    dZ = _to_tensor("dZ", dZ, g.device)
+    d = dZ.shape[1]
+    out = accounting.register(torch.zeros((rows, d), dtype=dZ.dtype, device=g.device))
+    tindex = g.src.data_ptr() if target == "src" else None
+    if out.numel():
+        _lib.check(_lib.load().gmp_extrema_bwd_copy(
+            arg.shape[0], d, _dtype_code(dZ), arg.data_ptr(), dZ.data_ptr(), _ld(dZ), tindex,
+            out.data_ptr(), d, _stream(g.device)), "gmp_extrema_bwd_copy")
+    return out
+
+
+# ----------------------------------------------------------------------------
+# fused edge_softmax (replaces the 4-dispatch composition of messaging.py:105-126)
+
+
+def edge_softmax_forward(g, scores):
+    """alpha = per-destination softmax of (m, H) scores, one fused row kernel."""
+    _require_cuda(g)
+    S = _as_matrix("scores", scores, g.num_edges, g.device)
+    H = S.shape[1]
+    accounting.log_dispatch("gspmm", g.uid, "edge_softmax", "softmax", "node_parallel",
+                            g.num_edges, H)
+    alpha = accounting.register(torch.empty((g.num_edges, H), dtype=S.dtype, device=g.device))
+    if alpha.numel():
+        adj = g.to_csc()
+        sched = adj.schedule()
+        _lib.check(_lib.load().gmp_edge_softmax_fwd(
+            ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), _dtype_code(S),
+            S.data_ptr(), _ld(S), H, alpha.data_ptr(), H, _stream(g.device)),
+            "gmp_edge_softmax_fwd")
+    return alpha
+
+
+def edge_softmax_backward(g, alpha, grad):
+    """ds = alpha * (grad - sum_{in-edges} alpha * grad), one fused row kernel."""
+    _require_cuda(g)
+    A = _as_matrix("alpha", alpha, g.num_edges, g.device)
+    Gr = _as_matrix("grad", grad, g.num_edges, g.device).to(A.dtype)
+    H = A.shape[1]
+    accounting.log_dispatch("gspmm", g.uid, "edge_softmax_bwd", "softmax", "node_parallel",
+                            g.num_edges, H)
+    ds = accounting.register(torch.empty((g.num_edges, H), dtype=A.dtype, device=g.device))
+    if ds.numel():
+        adj = g.to_csc()
+        sched = adj.schedule()
+        _lib.check(_lib.load().gmp_edge_softmax_bwd(
+            ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), _dtype_code(A),
+            A.data_ptr(), _ld(A), Gr.data_ptr(), _ld(Gr), H, ds.data_ptr(), H,
+            _stream(g.device)), "gmp_edge_softmax_bwd")
+    return ds

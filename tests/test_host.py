@@ -1,0 +1,198 @@
+"""Host-side logic on CPU: validation, graph indexes, caches, instrumentation.
+
+No kernel runs here; the graph lives on the CPU device, where every kernel
+entry point must refuse to run (there is no CPU fallback).
+"""
+
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1909_01315_b200 as G
+from paper_1909_01315_b200 import accounting, kernels
+from conftest import golden, golden_graph, to_np
+
+
+def cpu_graph(n, edges):
+    return G.build_graph(n, edges, device="cpu")
+
+
+def test_message_func_validation():
+    with pytest.raises(ValueError):
+        kernels.MessageFunc("mul", "src", "src")
+    with pytest.raises(ValueError):
+        kernels.MessageFunc("copy_lhs", "src", "dst")
+    with pytest.raises(ValueError):
+        kernels.MessageFunc("hypot", "src", "dst")
+    phis = kernels.builtin_message_funcs()
+    assert len(phis) == 30
+    assert phis[0].describe() == "copy_lhs(src)"
+    assert [p.describe() for p in phis[-3:]] == ["dot(src,dst)", "dot(src,edge)", "dot(dst,edge)"]
+
+
+def test_graph_validation_errors():
+    with pytest.raises(ValueError, match="outside"):
+        G.Graph(np.array([0, 5]), np.array([1, 1]), 3, device="cpu")
+    with pytest.raises(ValueError, match="negative"):
+        G.build_graph(3, [(0, -1)], device="cpu")
+    with pytest.raises(ValueError):
+        G.Graph(np.array([0, 1]), np.array([1]), 3, device="cpu")
+
+
+def test_adjacency_bit_exact_vs_reference():
+    gd = golden()
+    src, dst, n = golden_graph("idx")
+    g = G.from_arrays(src, dst, num_nodes=n, device="cpu")
+    for nm, adj in (("csc", g.to_csc()), ("csr", g.to_csr())):
+        indptr, indices, eids = adj.numpy()
+        assert np.array_equal(indptr, gd["idx/%s/indptr" % nm])
+        assert np.array_equal(indices, gd["idx/%s/indices" % nm])
+        assert np.array_equal(eids, gd["idx/%s/edge_ids" % nm])
+
+
+def test_reverse_shares_cache_pair():
+    g = cpu_graph(3, [(0, 2), (1, 2), (2, 0)])
+    rev = G.reverse(g)
+    assert G.reverse(rev) is g
+    assert rev.to_csc() is g.to_csr()
+    assert rev.to_csr() is g.to_csc()
+    assert g.adjacency_build_count == 2
+    rev.to_csc()
+    assert g.adjacency_build_count == 2
+    assert rev.uid != g.uid
+
+
+def test_concurrent_cache_build_is_single():
+    rng = np.random.default_rng(0)
+    g = G.from_arrays(rng.integers(0, 50, 500), rng.integers(0, 50, 500), 50, device="cpu")
+    barrier = threading.Barrier(8)
+    got = []
+
+    def run():
+        barrier.wait()
+        got.append(g.to_csc())
+
+    ts = [threading.Thread(target=run) for _ in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(a is got[0] for a in got)
+    assert g.adjacency_build_count == 1
+
+
+def test_degrees():
+    g = cpu_graph(3, [(0, 2), (1, 2), (2, 0)])
+    assert to_np(g.in_degrees()).tolist() == [1, 0, 2]
+    assert to_np(g.out_degrees()).tolist() == [1, 1, 1]
+    g.to_csc()
+    assert to_np(g.in_degrees([2, 0])).tolist() == [2, 1]
+    with pytest.raises(IndexError):
+        g.in_degrees([3])
+
+
+def test_kernels_refuse_cpu_graph():
+    g = cpu_graph(3, [(0, 2), (1, 2), (2, 0)])
+    x = np.ones((3, 1))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        G.gspmm(g, kernels.copy("src"), "sum", X=x)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        G.gsddmm(g, kernels.copy("src"), X=x)
+
+
+def test_validation_happens_before_device_check():
+    g = cpu_graph(3, [(0, 2), (1, 2), (2, 0)])
+    with pytest.raises(ValueError):
+        G.gspmm(g, kernels.add("src", "dst"), "sum", X=np.ones((3, 2)), Y=np.ones((3, 3)))
+    with pytest.raises(ValueError):
+        G.gspmm(g, kernels.mul("src", "edge"), "sum", X=np.ones((3, 1)))
+    with pytest.raises(ValueError):
+        G.gspmm(g, kernels.copy("src"), "sum", X=np.ones((4, 1)))
+    with pytest.raises(ValueError):
+        G.gsddmm(g, kernels.copy_rhs("edge"), W=np.ones((2, 1)))
+    with pytest.raises(ValueError):
+        G.gsddmm(g, kernels.dot("src", "dst"), X=np.ones((3, 2)), Y=np.ones((3, 3)))
+    with pytest.raises(ValueError):
+        G.gspmm(g, kernels.copy("src"), "sum", X=np.ones((3, 1)), strategy="warp")
+    with pytest.raises(ValueError):
+        G.gspmm(g, kernels.copy("src"), "median", X=np.ones((3, 1)))
+    with pytest.raises(ValueError, match="atomic"):
+        G.gsddmm(g, kernels.copy("src"), X=np.ones((3, 1)), strategy="edge_parallel_atomic")
+    with pytest.raises(ValueError):
+        G.gspmm(g, kernels.copy("src"), "sum", X=np.ones((3, 1)), strategy="node_parallel",
+                fmt="coo")
+    with pytest.raises(ValueError):
+        G.gspmm(g, kernels.copy("src"), "sum", X=np.ones((3,)))
+
+
+def test_select_format():
+    assert G.select_format("gspmm", "forward") == "csc"
+    assert G.select_format("gspmm", "backward") == "csc"
+    assert G.select_format("gsddmm") == "coo"
+    with pytest.raises(ValueError):
+        G.select_format("spmv")
+
+
+def test_allocation_meter_and_dispatch_log(tmp_path):
+    with pytest.raises(G.MemoryCapExceeded):
+        with accounting.track_allocations(cap_bytes=100):
+            accounting.register_bytes(101)
+    with accounting.track_allocations() as meter:
+        accounting.register(torch.zeros(10, 4))
+        accounting.release_bytes(80)
+    assert meter.peak_bytes == 160 and meter.current_bytes == 80
+    assert meter.largest_single_bytes == 160
+    with G.capture_dispatch() as log:
+        accounting.log_dispatch("gspmm", 7, "copy_lhs(src)", "sum", "node_parallel", 3, 2)
+    path = tmp_path / "d.log"
+    accounting.write_dispatch_log(path, log)
+    assert path.read_text().strip() == "gspmm,7,copy_lhs(src),sum,node_parallel,3,2"
+
+
+def test_feature_dict():
+    fd = G.FeatureDict(3, device="cpu")
+    fd["h"] = np.array([1.0, 2.0, 3.0])
+    assert tuple(fd["h"].shape) == (3, 1)
+    assert "h" in fd and len(fd) == 1
+    with pytest.raises(ValueError):
+        fd["x"] = np.ones((4, 1))
+    with pytest.raises(ValueError):
+        fd["x"] = np.array([1.0, np.inf, 0.0])
+    with pytest.raises(KeyError, match="have: h"):
+        fd["nope"]
+    with pytest.raises(ValueError):
+        fd[""] = np.ones((3, 1))
+    del fd["h"]
+    assert len(fd) == 0
+
+
+def test_messaging_host_errors():
+    g = cpu_graph(3, [(0, 2), (1, 2), (2, 0)])
+    nd = G.FeatureDict(3, device="cpu")
+    nd["h"] = np.ones((3, 1))
+    with pytest.raises(ValueError, match="edata"):
+        G.apply_edges(g, G.msg("copy", G.src("h")), nd, out="m")
+    with pytest.raises(ValueError, match="edata"):
+        G.edge_softmax(g, "s")
+    m = G.msg("copy_rhs", G.edge("w"))
+    assert m.lhs is None and m.rhs.name == "w"
+
+
+def test_generators_match_reference():
+    gd = golden()
+    g = G.power_law(400, 6, seed=3, device="cpu")
+    assert np.array_equal(to_np(g.src), gd["gen/power_law_400_6_3/src"])
+    assert np.array_equal(to_np(g.dst), gd["gen/power_law_400_6_3/dst"])
+    spec = G.generators.parse_graph_spec("power_law:n=100,deg=3,seed=4")
+    assert spec == G.GenSpec("power_law", 100, 3.0, 4)
+    with pytest.raises(ValueError):
+        G.generators.parse_graph_spec("chain:deg=3")
+
+
+def test_rmat_cpu_shape_and_range():
+    s, d = G.generators.rmat_edges(1000, 5000, seed=1, device="cpu")
+    assert s.numel() == 5000 and int(s.max()) < 1000 and int(d.max()) < 1000
+    s2, _ = G.generators.rmat_edges(1000, 5000, seed=1, device="cpu")
+    assert torch.equal(s, s2)
