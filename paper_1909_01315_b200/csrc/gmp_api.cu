@@ -4,6 +4,7 @@
 // (kernels.py:224-252, _operands_for) so that a caller gets the same class of
 // error for the same mistake; shape checks that need row counts stay in the
 // Python mirror (paper_1909_01315_b200/kernels.py), which owns the tensors.
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -17,7 +18,7 @@
 
 namespace gmp {
 template <int OP>
-cudaError_t launch_spmm_rows(int, int, int, int, const SpmmArgs&, int64_t, cudaStream_t);
+cudaError_t launch_spmm_rows(int, int, int, int, const SpmmArgs&, int64_t, cudaStream_t);  // (f64, rho, V, mode pair)
 cudaError_t launch_route_extrema(int, int64_t, int32_t, const int64_t*, const void*, int64_t, void*,
                                  int64_t, cudaStream_t);
 cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const void*, int64_t,
@@ -148,7 +149,8 @@ int kernel_op(int op) {
 }
 
 // Column-tile width: the whole row when the gathered source slice fits the
-// L2 budget, otherwise the widest slice that does (>= one 128 B line).
+// L2 budget, otherwise the widest multiple of one full warp pass (32 * V
+// columns) that does; then balanced over the resulting tile count.
 int pick_tile(const gmp_tuning* tun, int d_out, int V, size_t F, int64_t n_src_rows, bool src_full,
               int max_tw) {
   int tw;
@@ -161,20 +163,29 @@ int pick_tile(const gmp_tuning* tun, int d_out, int V, size_t F, int64_t n_src_r
       const int64_t per_col = n_src_rows * (int64_t)F;
       const int64_t fit = per_col > 0 ? budget / per_col : d_out;
       if (fit < d_out) {
-        const int min_cols = (int)(128 / F);
-        int64_t c = fit < min_cols ? min_cols : fit;
-        tw = (int)((c / V) * V);
-        if (tw < V) tw = V;
+        const int unit = 32 * V;
+        tw = (int)std::max<int64_t>(unit, (fit / unit) * unit);
       }
     }
   }
   if (tw > max_tw) tw = max_tw;
-  if (tw > d_out) tw = d_out;
+  if (tw >= d_out) return d_out;
   if (tw < 1) tw = 1;
   const int ntiles = (d_out + tw - 1) / tw;
   tw = (d_out + ntiles - 1) / ntiles;
   tw = ((tw + V - 1) / V) * V;
   return tw;
+}
+
+RowOperand row_operand(const Opnd& o) {
+  RowOperand r{};
+  if (!o.present) return r;
+  r.data = o.dev.data;
+  r.ld = (uint32_t)o.dev.ld;
+  r.from_eid = o.dev.target == GMP_EDGE;
+  r.bcast = o.dev.bcast;
+  r.mode = o.dev.target == GMP_DST ? M_HOIST : (o.dev.bcast ? M_SCALAR : M_FULL);
+  return r;
 }
 
 }  // namespace
@@ -242,6 +253,8 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
   if (sched && sched->order == nullptr && sched->n_heavy > 0)
     return fail(GMP_EINVAL, "schedule has heavy rows but no order");
 
+  if ((lhs && lhs->ld >= (1ll << 32)) || (rhs && rhs->ld >= (1ll << 32)))
+    return fail(GMP_EUNSUPPORTED, "operand leading dimension must be < 2^32");
   const size_t F = dtype == GMP_F64 ? 8 : 4;
   const int kop = kernel_op(op);
   const int krho = rho == GMP_MAX ? RHO_MAX : (rho == GMP_MIN ? RHO_MIN : RHO_SUM);
@@ -274,26 +287,40 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
   const int V = pick_v(F, d_out, ops, 2, Z, ldz, ext ? arg : nullptr);
   const bool src_full = (ops[0].dev.target == GMP_SRC && !ops[0].dev.bcast) ||
                         (ops[1].present && ops[1].dev.target == GMP_SRC && !ops[1].dev.bcast);
-  const int max_tw = 32 * V * 2;
+  const int max_tw = 32 * V;
   const int tw = pick_tile(tuning, d_out, V, F, adj->n_rows, src_full, max_tw);
   const int G = std::min(32, next_pow2((tw + V - 1) / V));
-  const int P = (tw + G * V - 1) / (G * V);
   const int ntiles = (d_out + tw - 1) / tw;
 
   SpmmArgs a{};
   a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
   a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.blocks_per_tile = bpt;
   a.d_out = d_out; a.tile_cols = tw; a.g_log2 = log2i(G); a.mean = rho == GMP_MEAN;
-  a.lhs = ops[0].dev; a.rhs = ops[1].dev;
+  a.lhs = row_operand(ops[0]);
+  a.rhs = row_operand(ops[1]);
+  // compile-time mode pair for the hot shapes; add / mul commute, so a
+  // gathered operand on the right is swapped to the left (bit-identical)
+  int mp = MP_GEN;
+  if (F == 4) {
+    if (kop == OP_COPY) {
+      mp = a.lhs.mode == M_FULL ? MP_F : MP_GEN;
+    } else if (kop == OP_ADD || kop == OP_MUL || kop == OP_SUB) {
+      if (a.lhs.mode != M_FULL && a.rhs.mode == M_FULL && kop != OP_SUB) std::swap(a.lhs, a.rhs);
+      if (a.lhs.mode == M_FULL)
+        mp = a.rhs.mode == M_FULL ? MP_FF : (a.rhs.mode == M_SCALAR ? MP_FS : MP_FH);
+    }
+  }
+  a.need_eid = ext || (a.lhs.from_eid && a.lhs.mode != M_HOIST) ||
+               (ops[1].present && a.rhs.from_eid && a.rhs.mode != M_HOIST);
   a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts; a.err_pos = err_pos;
   const int64_t grid = bpt * ntiles;
   if (grid >= (1ll << 31)) return fail(GMP_EUNSUPPORTED, "grid too large");
   switch (kop) {
-    case OP_COPY: e = launch_spmm_rows<OP_COPY>(F == 8, krho, V, P, a, grid, s); break;
-    case OP_ADD: e = launch_spmm_rows<OP_ADD>(F == 8, krho, V, P, a, grid, s); break;
-    case OP_SUB: e = launch_spmm_rows<OP_SUB>(F == 8, krho, V, P, a, grid, s); break;
-    case OP_MUL: e = launch_spmm_rows<OP_MUL>(F == 8, krho, V, P, a, grid, s); break;
-    default: e = launch_spmm_rows<OP_DIV>(F == 8, krho, V, P, a, grid, s); break;
+    case OP_COPY: e = launch_spmm_rows<OP_COPY>(F == 8, krho, V, mp, a, grid, s); break;
+    case OP_ADD: e = launch_spmm_rows<OP_ADD>(F == 8, krho, V, mp, a, grid, s); break;
+    case OP_SUB: e = launch_spmm_rows<OP_SUB>(F == 8, krho, V, mp, a, grid, s); break;
+    case OP_MUL: e = launch_spmm_rows<OP_MUL>(F == 8, krho, V, mp, a, grid, s); break;
+    default: e = launch_spmm_rows<OP_DIV>(F == 8, krho, V, mp, a, grid, s); break;
   }
   g_launches++;
   return cuda_status(e, "gmp_gspmm");

@@ -7,8 +7,8 @@
 // with the message formed in registers and never materialised.
 //
 // Work decomposition:
-//  * columns are split into tiles of `tile_cols` (the reference's
-//    feature_parallel column split, kernels.py:485-513) so that one column
+//  * columns are split into tiles of <= 32*V columns (the reference's
+//    feature_parallel column split, kernels.py:485-513), sized so one column
 //    slice of the gathered source matrix stays L2-resident; tiles are the
 //    slowest-varying grid index, so concurrently running CTAs share a slice;
 //  * rows come in degree-descending order (gmp_sched). The first n_heavy rows
@@ -16,18 +16,45 @@
 //    32-edge batches, partials merged through shared memory in warp order);
 //    the rest are reduced by one warp each;
 //  * inside a warp, 32 lanes = E edge slots x G feature lanes; each feature
-//    lane owns P vectors of V elements (128/64-bit loads). Edge indices are
-//    loaded 32 at a time, coalesced, and broadcast by shuffle; the next batch
-//    is prefetched while the current one is gathered.
+//    lane owns one V-vector (128/64-bit loads). Edge indices (and per-edge
+//    scalar operands such as an attention weight) are loaded 32 at a time,
+//    coalesced, ahead of use, and broadcast by shuffle. The gather loop is
+//    branch-free: masked lanes load a clamped in-bounds address and select 0;
+//  * operand access modes (per-edge vector gather / per-edge scalar /
+//    row-constant) are template parameters for the hot combinations
+//    (copy_u/copy_e, u_op_e, u_op_v, e_op_v) and runtime for the rest;
 //  * slot partials are combined by a fixed xor-shuffle tree: results are
 //    deterministic run to run.
+//
+// Numerics: fp32 sums are carried as an exact
+// compensated pair (TwoSum / TwoProduct on packed FADD2/FFMA2) and folded
+// into an fp64 accumulator every 32 edges - equivalent to fp64 accumulation
+// of the exact fp64 messages the reference forms, without per-element
+// F2F.F64.F32 conversions (those run on the slow XU pipe). max/min of copy
+// messages compare the fp32 values directly (exact); max/min of binary
+// messages compare the fp64 message, so arg edges equal the reference's.
 #pragma once
+
+#include <type_traits>
 
 #include "gmp_common.cuh"
 
 namespace gmp {
 
 constexpr int kWarpsPerCta = 8;
+
+// operand access modes inside the row kernel
+enum { M_FULL = 0, M_SCALAR = 1, M_HOIST = 2, M_NONE = 3 };
+// compile-time (lhs, rhs) mode pairs; MP_GEN reads the modes at run time
+enum { MP_F = 0, MP_FF = 1, MP_FS = 2, MP_FH = 3, MP_GEN = 4 };
+
+struct RowOperand {
+  const void* data;
+  uint32_t ld;
+  int32_t mode;      // M_FULL / M_SCALAR / M_HOIST
+  int32_t from_eid;  // gathered by edge id (EDGE target) instead of neighbour id (SRC target)
+  int32_t bcast;     // hoisted operand is a single column
+};
 
 struct SpmmArgs {
   const int64_t* indptr;
@@ -41,7 +68,8 @@ struct SpmmArgs {
   int32_t tile_cols;
   int32_t g_log2;  // feature lanes per edge slot = 1 << g_log2
   int32_t mean;
-  OperandDev lhs, rhs;
+  int32_t need_eid;
+  RowOperand lhs, rhs;
   void* Z;
   int64_t ldz;
   int64_t* arg;
@@ -49,182 +77,356 @@ struct SpmmArgs {
   int32_t* err_pos;
 };
 
-template <typename T, int V, int P>
-__device__ __forceinline__ void load_hoisted(const OperandDev& o, int64_t row, const int (&colv)[P],
-                                             const bool (&valid)[P], T (&h)[P][V]) {
-  const T* base = static_cast<const T*>(o.data) + row * o.ld;
+// ---- accumulation policies ---------------------------------------------------
+
+enum { POL_COMP = 0, POL_DBL = 1, POL_EXT_T = 2, POL_EXT_D = 3 };
+
+template <typename T, int OP, int RHO>
+struct Policy {
+  static constexpr int value =
+      (RHO != RHO_SUM)
+          ? ((OP == OP_COPY || sizeof(T) == 8) ? POL_EXT_T : POL_EXT_D)
+          : ((sizeof(T) == 4 && OP != OP_DIV) ? POL_COMP : POL_DBL);
+};
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// s + c += x exactly (TwoSum, Knuth); packed fp32x2.
+__device__ __forceinline__ void two_sum2(float2& s, float2& c, float2 x) {
+  const float2 m1 = f2(-1.f, -1.f);
+  const float2 t = __fadd2_rn(s, x);
+  const float2 bb = __ffma2_rn(s, m1, t);                      // t - s
+  const float2 e1 = __ffma2_rn(__ffma2_rn(bb, m1, t), m1, s);  // s - (t - bb)
+  const float2 e2 = __ffma2_rn(bb, m1, x);                     // x - bb
+  c = __fadd2_rn(c, __fadd2_rn(e1, e2));
+  s = t;
+}
+
+__device__ __forceinline__ void two_sum1(float& s, float& c, float x) {
+  const float t = __fadd_rn(s, x);
+  const float bb = __fsub_rn(t, s);
+  const float e = __fadd_rn(__fsub_rn(s, __fsub_rn(t, bb)), __fsub_rn(x, bb));
+  c = __fadd_rn(c, e);
+  s = t;
+}
+
+// Per-lane accumulator for the V output elements a feature lane owns.
+template <typename T, int OP, int RHO, int V>
+struct RowAcc {
+  static constexpr int POL = Policy<T, OP, RHO>::value;
+  using ExtT = typename std::conditional<POL == POL_EXT_D, double, T>::type;
+  double acc[V];
+  float s[V], c[V];
+  ExtT cur[V];
+  int32_t arg[V];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      acc[k] = 0.0;
+      s[k] = 0.f;
+      c[k] = 0.f;
+      cur[k] = (ExtT)ext_init<RHO == RHO_SUM ? RHO_MAX : RHO>();
+      arg[k] = 0x7fffffff;
+    }
+  }
+
+  // fold the compensated fp32 pair into fp64 (every <= 32 edges)
+  __device__ __forceinline__ void fold() {
+    if constexpr (POL == POL_COMP) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        acc[k] += (double)s[k];
+        acc[k] += (double)c[k];
+        s[k] = 0.f;
+        c[k] = 0.f;
+      }
+    }
+  }
+
+  // add the message op(a, b) of one edge; masked lanes carry zeros for the
+  // sum policies and are excluded by `ok` for extrema
+  __device__ __forceinline__ void add(const T (&a)[V], const T (&b)[V], bool ok, int32_t e) {
+    if constexpr (POL == POL_COMP) {
+      if constexpr (V == 1) {
+        const float x = (float)a[0], y = (float)b[0];
+        if constexpr (OP == OP_COPY) {
+          two_sum1(s[0], c[0], x);
+        } else if constexpr (OP == OP_MUL) {
+          const float pr = __fmul_rn(x, y);
+          two_sum1(s[0], c[0], pr);
+          c[0] = __fadd_rn(c[0], __fmaf_rn(x, y, -pr));
+        } else {  // ADD / SUB: the exact message is itself a TwoSum pair
+          const float yy = OP == OP_SUB ? -y : y;
+          const float t = __fadd_rn(x, yy);
+          const float bb = __fsub_rn(t, x);
+          const float r = __fadd_rn(__fsub_rn(x, __fsub_rn(t, bb)), __fsub_rn(yy, bb));
+          two_sum1(s[0], c[0], t);
+          c[0] = __fadd_rn(c[0], r);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < V; k += 2) {
+          float2 S = f2(s[k], s[k + 1]), C = f2(c[k], c[k + 1]);
+          const float2 x = f2((float)a[k], (float)a[k + 1]);
+          if constexpr (OP == OP_COPY) {
+            two_sum2(S, C, x);
+          } else if constexpr (OP == OP_MUL) {
+            const float2 y = f2((float)b[k], (float)b[k + 1]);
+            const float2 pr = __fmul2_rn(x, y);
+            two_sum2(S, C, pr);
+            C = __fadd2_rn(C, __ffma2_rn(x, y, f2(-pr.x, -pr.y)));
+          } else {
+            float2 y = f2((float)b[k], (float)b[k + 1]);
+            if constexpr (OP == OP_SUB) y = f2(-y.x, -y.y);
+            // exact message x + y = t + r, then accumulate both parts
+            const float2 m1 = f2(-1.f, -1.f);
+            const float2 t = __fadd2_rn(x, y);
+            const float2 bb = __ffma2_rn(x, m1, t);
+            const float2 r = __fadd2_rn(__ffma2_rn(__ffma2_rn(bb, m1, t), m1, x),
+                                        __ffma2_rn(bb, m1, y));
+            two_sum2(S, C, t);
+            C = __fadd2_rn(C, r);
+          }
+          s[k] = S.x; s[k + 1] = S.y;
+          c[k] = C.x; c[k + 1] = C.y;
+        }
+      }
+    } else if constexpr (POL == POL_DBL) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] += apply_op<OP>((double)a[k], (double)b[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        ExtT x;
+        if constexpr (POL == POL_EXT_T && OP == OP_COPY) x = a[k];
+        else x = (ExtT)apply_op<OP>((double)a[k], (double)b[k]);
+        const bool better = (RHO == RHO_MAX) ? (x > cur[k]) : (x < cur[k]);
+        const bool tie = (x == cur[k]) && (e < arg[k]);
+        if (ok && better) cur[k] = x;
+        if (ok && (better || tie)) arg[k] = e;
+      }
+    }
+  }
+
+  // combine with the partial of another lane/warp (fixed order => deterministic)
+  __device__ __forceinline__ void merge(int k, double oacc, ExtT ocur, int32_t oarg) {
+    if constexpr (POL == POL_COMP || POL == POL_DBL) {
+      acc[k] += oacc;
+    } else {
+      const bool better = (RHO == RHO_MAX) ? (ocur > cur[k]) : (ocur < cur[k]);
+      if (better) { cur[k] = ocur; arg[k] = oarg; }
+      else if (ocur == cur[k] && oarg < arg[k]) arg[k] = oarg;
+    }
+  }
+
+  __device__ __forceinline__ void combine_slots(int g_log2) {
+    for (int off = 1 << g_log2; off < 32; off <<= 1) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if constexpr (POL == POL_COMP || POL == POL_DBL) {
+          merge(k, __shfl_xor_sync(kFull, acc[k], off), ExtT(0), 0);
+        } else {
+          const ExtT oc = __shfl_xor_sync(kFull, cur[k], off);
+          const int32_t oa = __shfl_xor_sync(kFull, arg[k], off);
+          merge(k, 0.0, oc, oa);
+        }
+      }
+    }
+  }
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void load_hoisted(const RowOperand& o, int64_t row, int col, bool valid,
+                                             T (&h)[V]) {
+  const T* base = static_cast<const T*>(o.data) + (uint64_t)row * o.ld;
   if (o.bcast) {
     const T s = __ldg(base);
 #pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int k = 0; k < V; ++k) h[p][k] = s;
+    for (int k = 0; k < V; ++k) h[k] = s;
   } else {
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      if (valid[p]) load_vec<T, V>(base + colv[p], h[p]);
-      else
-#pragma unroll
-        for (int k = 0; k < V; ++k) h[p][k] = T(0);
-    }
+    for (int k = 0; k < V; ++k) h[k] = T(0);
+    if (valid) load_vec<T, V>(base + col, h);
   }
 }
 
-template <typename T, int V, int P>
-__device__ __forceinline__ void load_operand(const OperandDev& o, int32_t nbr, int32_t eid,
-                                             const int (&colv)[P], const bool (&valid)[P],
-                                             const T (&hoisted)[P][V], T (&out)[P][V]) {
-  if (o.target == T_DST) {
+template <typename T>
+__device__ __forceinline__ T scalar_at(const RowOperand& o, uint32_t row) {
+  return __ldg(static_cast<const T*>(o.data) + (uint64_t)row * o.ld);
+}
+
+// Branch-free vector gather: `colbase` already points at this lane's (clamped,
+// in-bounds) column of row 0; masked lanes read row 0 and select zero.
+template <typename T, int V>
+__device__ __forceinline__ void gather_full(const T* colbase, uint32_t ld_bytes, uint32_t row,
+                                            bool use, T (&out)[V]) {
+  const T* p = reinterpret_cast<const T*>(reinterpret_cast<const char*>(colbase) +
+                                          (uint64_t)(use ? row : 0u) * ld_bytes);
+  load_vec<T, V>(p, out);
 #pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int k = 0; k < V; ++k) out[p][k] = hoisted[p][k];
-    return;
-  }
-  const int64_t r = (o.target == T_SRC) ? nbr : eid;
-  const T* base = static_cast<const T*>(o.data) + r * o.ld;
-  if (o.bcast) {
-    const T s = __ldg(base);
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int k = 0; k < V; ++k) out[p][k] = s;
-  } else {
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-      if (valid[p]) load_vec<T, V>(base + colv[p], out[p]);
-  }
+  for (int k = 0; k < V; ++k) out[k] = use ? out[k] : T(0);
 }
 
 // Accumulate the messages of edges [pb, pe) of one row owned by this warp:
 // 32-edge batches starting at pb + first, advancing by `stride` edges.
-template <typename T, int OP, int RHO, int V, int P, int U>
+template <typename T, int OP, int RHO, int V, int MP, int U>
 __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, int64_t pe,
                                                 int64_t first, int64_t stride, int lane, int slot,
-                                                int E, const int (&colv)[P], const bool (&valid)[P],
-                                                const T (&ha)[P][V], const T (&hb)[P][V],
-                                                double (&acc)[P][V], int32_t (&arg)[P][V]) {
+                                                int E, int col, bool valid, const T (&ha)[V],
+                                                const T (&hb)[V], RowAcc<T, OP, RHO, V>& acc) {
   constexpr bool BIN = OP != OP_COPY;
-  const bool need_eid = (a.lhs.target == T_EDGE) || (BIN && a.rhs.target == T_EDGE) ||
-                        (RHO != RHO_SUM);
   const int32_t* __restrict__ indices = a.indices;
   const int32_t* __restrict__ eids = a.eids;
+  const bool need_eid = a.need_eid;
+  // operand modes: compile-time unless MP_GEN
+  const int lm = (MP == MP_GEN) ? a.lhs.mode : M_FULL;
+  const int rm = !BIN ? M_NONE
+                      : (MP == MP_FF ? M_FULL
+                                     : (MP == MP_FS ? M_SCALAR
+                                                    : (MP == MP_FH ? M_HOIST : a.rhs.mode)));
+  const bool l_eid = a.lhs.from_eid, r_eid = a.rhs.from_eid;
+  // lane column base pointers (clamped in-bounds for masked columns)
+  const int ccol = valid ? col : 0;
+  const T* lcol = static_cast<const T*>(a.lhs.data) + ccol;
+  const T* rcol = BIN ? static_cast<const T*>(a.rhs.data) + ccol : nullptr;
+  const uint32_t lld = a.lhs.ld * (uint32_t)sizeof(T);
+  const uint32_t rld = a.rhs.ld * (uint32_t)sizeof(T);
 
+  // two-deep index prefetch, one-deep per-edge scalar prefetch
   int64_t base = pb + first;
-  int nb = 0, eb = 0;
-  if (base < pe && lane < pe - base) {
-    nb = __ldg(indices + base + lane);
-    if (need_eid) eb = __ldg(eids + base + lane);
+  int32_t nb0 = 0, eb0 = 0, nb1 = 0, eb1 = 0;
+  if (base + lane < pe) {
+    nb0 = __ldg(indices + base + lane);
+    if (need_eid) eb0 = __ldg(eids + base + lane);
   }
+  if (base + stride + lane < pe) {
+    nb1 = __ldg(indices + base + stride + lane);
+    if (need_eid) eb1 = __ldg(eids + base + stride + lane);
+  }
+  T sa0 = T(0), sb0 = T(0);
+  if (base + lane < pe) {
+    if (lm == M_SCALAR) sa0 = scalar_at<T>(a.lhs, l_eid ? eb0 : nb0);
+    if (rm == M_SCALAR) sb0 = scalar_at<T>(a.rhs, r_eid ? eb0 : nb0);
+  }
+  int since_fold = 0;
   for (; base < pe; base += stride) {
     const int cnt = batch_count(pe - base);
-    // prefetch the next batch's indices while this one is gathered
-    const int64_t nbase = base + stride;
-    int nb_next = 0, eb_next = 0;
-    if (nbase < pe && lane < pe - nbase) {
-      nb_next = __ldg(indices + nbase + lane);
-      if (need_eid) eb_next = __ldg(eids + nbase + lane);
+    // prefetch: indices two batches ahead, scalars one batch ahead
+    const int64_t b2 = base + 2 * stride;
+    int32_t nb2 = 0, eb2 = 0;
+    if (b2 + lane < pe) {
+      nb2 = __ldg(indices + b2 + lane);
+      if (need_eid) eb2 = __ldg(eids + b2 + lane);
     }
+    T sa1 = T(0), sb1 = T(0);
+    if (base + stride + lane < pe) {
+      if (lm == M_SCALAR) sa1 = scalar_at<T>(a.lhs, l_eid ? eb1 : nb1);
+      if (rm == M_SCALAR) sb1 = scalar_at<T>(a.rhs, r_eid ? eb1 : nb1);
+    }
+    const uint32_t ra_lane = l_eid ? eb0 : nb0;
+    const uint32_t rb_lane = r_eid ? eb0 : nb0;
+#pragma unroll 1
     for (int t = 0; t < cnt; t += E * U) {
-      T va[U][P][V];
-      T vb[U][P][V];
+      T va[U][V];
+      T vb[U][V];
       int32_t ee[U];
       bool ok[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int j = t + slot + E * u;
         ok[u] = j < cnt;
-        const int src_lane = j & 31;
-        const int32_t uu = __shfl_sync(kFull, nb, src_lane);
-        ee[u] = need_eid ? __shfl_sync(kFull, eb, src_lane) : 0;
-        if (ok[u]) {
-          load_operand<T, V, P>(a.lhs, uu, ee[u], colv, valid, ha, va[u]);
-          if constexpr (BIN) load_operand<T, V, P>(a.rhs, uu, ee[u], colv, valid, hb, vb[u]);
+        const int sl = j & 31;
+        const bool use = ok[u] && valid;
+        ee[u] = (RHO != RHO_SUM) ? __shfl_sync(kFull, eb0, sl) : 0;
+        // lhs
+        if (lm == M_FULL) {
+          gather_full<T, V>(lcol, lld, __shfl_sync(kFull, ra_lane, sl), use, va[u]);
+        } else {
+          const T sa = (lm == M_SCALAR) ? __shfl_sync(kFull, sa0, sl) : T(0);
+#pragma unroll
+          for (int k = 0; k < V; ++k) va[u][k] = (lm == M_SCALAR) ? sa : ha[k];
+        }
+        // rhs
+        if (rm == M_FULL) {
+          gather_full<T, V>(rcol, rld, __shfl_sync(kFull, rb_lane, sl), use, vb[u]);
+        } else if (rm == M_NONE) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) vb[u][k] = T(0);
+        } else {
+          const T sb = (rm == M_SCALAR) ? __shfl_sync(kFull, sb0, sl) : T(0);
+#pragma unroll
+          for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (!ok[u]) continue;
+        const bool use = ok[u] && valid;
         if constexpr (OP == OP_DIV) {
           bool zero = false;
 #pragma unroll
-          for (int p = 0; p < P; ++p)
-            if (valid[p])
-#pragma unroll
-              for (int k = 0; k < V; ++k) zero |= (vb[u][p][k] == T(0));
-          if (zero) atomicMin(a.err_pos, (int32_t)(base + t + slot + E * u));
+          for (int k = 0; k < V; ++k) zero |= valid && (vb[u][k] == T(0));
+          if (ok[u] && zero) atomicMin(a.err_pos, (int32_t)(base + t + slot + E * u));
         }
+        // masked lanes contribute exactly nothing: a = 0 and b = 0 (1 for div)
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          if (!valid[p]) continue;
-#pragma unroll
-          for (int k = 0; k < V; ++k) {
-            const double x = apply_op<OP>((double)va[u][p][k], BIN ? (double)vb[u][p][k] : 0.0);
-            if constexpr (RHO == RHO_SUM) acc[p][k] += x;
-            else ext_update<RHO>(acc[p][k], arg[p][k], x, ee[u]);
-          }
+        for (int k = 0; k < V; ++k) {
+          va[u][k] = use ? va[u][k] : T(0);
+          vb[u][k] = use ? vb[u][k] : (OP == OP_DIV ? T(1) : T(0));
         }
+        acc.add(va[u], vb[u], ok[u], ee[u]);
       }
     }
-    nb = nb_next;
-    eb = eb_next;
+    if (++since_fold >= E) {  // each slot has seen <= 32 edges since the last fold
+      acc.fold();
+      since_fold = 0;
+    }
+    nb0 = nb1; eb0 = eb1; nb1 = nb2; eb1 = eb2;
+    sa0 = sa1; sb0 = sb1;
   }
+  acc.fold();
 }
 
-template <int RHO, int V, int P>
-__device__ __forceinline__ void combine_slots(int g_log2, double (&acc)[P][V], int32_t (&arg)[P][V]) {
-  for (int off = 1 << g_log2; off < 32; off <<= 1) {
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const double o = shfl_xor_d(acc[p][k], off);
-        if constexpr (RHO == RHO_SUM) {
-          acc[p][k] += o;
-        } else {
-          const int32_t oa = __shfl_xor_sync(kFull, arg[p][k], off);
-          ext_update<RHO>(acc[p][k], arg[p][k], o, oa);
-        }
-      }
-  }
-}
-
-template <typename T, int RHO, int V, int P>
-__device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_t deg,
-                                          const int (&colv)[P], const bool (&valid)[P],
-                                          const double (&acc)[P][V], const int32_t (&arg)[P][V]) {
+template <typename T, int OP, int RHO, int V>
+__device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_t deg, int col,
+                                          bool valid, const RowAcc<T, OP, RHO, V>& acc) {
+  if (!valid) return;
   T* z = static_cast<T*>(a.Z) + row * a.ldz;
+  T out[V];
+  if constexpr (RHO == RHO_SUM) {
 #pragma unroll
-  for (int p = 0; p < P; ++p) {
-    if (!valid[p]) continue;
-    T out[V];
-    if constexpr (RHO == RHO_SUM) {
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        double v = acc[p][k];
-        if (a.mean && deg > 0) v = v / (double)deg;  // kernels.py:719-722
-        out[k] = (T)v;
-      }
-      store_vec<T, V>(z + colv[p], out);
-    } else {
-      int32_t ar[V];
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        out[k] = deg > 0 ? (T)acc[p][k] : T(0);
-        ar[k] = deg > 0 ? arg[p][k] : -1;
-      }
-      store_vec<T, V>(z + colv[p], out);
-      store_arg<V>(a.arg + row * (int64_t)a.d_out + colv[p], ar);
+    for (int k = 0; k < V; ++k) {
+      double v = acc.acc[k];
+      if (a.mean && deg > 0) v = v / (double)deg;  // kernels.py:719-722
+      out[k] = (T)v;
     }
+    store_vec<T, V>(z + col, out);
+  } else {
+    int32_t ar[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      out[k] = deg > 0 ? (T)acc.cur[k] : T(0);
+      ar[k] = deg > 0 ? acc.arg[k] : -1;
+    }
+    store_vec<T, V>(z + col, out);
+    store_arg<V>(a.arg + row * (int64_t)a.d_out + col, ar);
   }
 }
 
-template <typename T, int OP, int RHO, int V, int P>
+template <int V>
+struct Unroll {
+  static constexpr int value = V == 4 ? 4 : 8;
+};
+
+template <typename T, int OP, int RHO, int V, int MP>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 spmm_rows_kernel(const SpmmArgs a) {
-  constexpr int U = (16 / (P * V)) < 2 ? 2 : (16 / (P * V));
-  constexpr int kCols = 32 * V * P;  // widest tile one warp covers
-  __shared__ double s_acc[kWarpsPerCta][kCols];
+  using Acc = RowAcc<T, OP, RHO, V>;
+  using ExtT = typename Acc::ExtT;
+  constexpr int U = Unroll<V>::value;
+  constexpr int kCols = 32 * V;  // widest tile one warp covers
+  __shared__ double s_acc[RHO == RHO_SUM ? kWarpsPerCta : 1][kCols];
+  __shared__ ExtT s_cur[RHO == RHO_SUM ? 1 : kWarpsPerCta][kCols];
   __shared__ int32_t s_arg[RHO == RHO_SUM ? 1 : kWarpsPerCta][kCols];
 
   const int64_t bid = blockIdx.x;
@@ -251,122 +453,117 @@ spmm_rows_kernel(const SpmmArgs a) {
   const int64_t pb = a.indptr[row];
   const int64_t pe = a.indptr[row + 1];
   const int64_t deg = pe - pb;
+  const int col = c0 + gl * V;
+  const bool valid = col < c1;
 
-  int colv[P];
-  bool valid[P];
+  T ha[V], hb[V];
 #pragma unroll
-  for (int p = 0; p < P; ++p) {
-    colv[p] = c0 + (gl + G * p) * V;
-    valid[p] = colv[p] < c1;
-  }
-
-  T ha[P][V], hb[P][V];
-  if (a.lhs.target == T_DST && deg > 0) load_hoisted<T, V, P>(a.lhs, row, colv, valid, ha);
-  if (OP != OP_COPY && a.rhs.target == T_DST && deg > 0) {
-    load_hoisted<T, V, P>(a.rhs, row, colv, valid, hb);
+  for (int k = 0; k < V; ++k) ha[k] = hb[k] = T(0);
+  if (MP == MP_GEN && a.lhs.mode == M_HOIST && deg > 0) load_hoisted<T, V>(a.lhs, row, col, valid, ha);
+  if (OP != OP_COPY && (MP == MP_FH || (MP == MP_GEN && a.rhs.mode == M_HOIST)) && deg > 0) {
+    load_hoisted<T, V>(a.rhs, row, col, valid, hb);
     if constexpr (OP == OP_DIV) {
       bool zero = false;
 #pragma unroll
-      for (int p = 0; p < P; ++p)
-        if (valid[p])
-#pragma unroll
-          for (int k = 0; k < V; ++k) zero |= (hb[p][k] == T(0));
+      for (int k = 0; k < V; ++k) zero |= valid && (hb[k] == T(0));
       if (zero) atomicMin(a.err_pos, (int32_t)pb);
     }
   }
 
-  double acc[P][V];
-  int32_t arg[P][V];
-#pragma unroll
-  for (int p = 0; p < P; ++p)
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      acc[p][k] = (RHO == RHO_SUM) ? 0.0 : ext_init<RHO>();
-      arg[p][k] = 0x7fffffff;
-    }
-
+  Acc acc;
+  acc.init();
   if (heavy) {
-    spmm_accumulate<T, OP, RHO, V, P, U>(a, pb, pe, (int64_t)warp * 32, 32 * kWarpsPerCta, lane,
-                                         slot, E, colv, valid, ha, hb, acc, arg);
+    spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, (int64_t)warp * 32, 32 * kWarpsPerCta, lane,
+                                          slot, E, col, valid, ha, hb, acc);
   } else {
-    spmm_accumulate<T, OP, RHO, V, P, U>(a, pb, pe, 0, 32, lane, slot, E, colv, valid, ha, hb,
-                                         acc, arg);
+    spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, 0, 32, lane, slot, E, col, valid, ha, hb,
+                                          acc);
   }
-  combine_slots<RHO, V, P>(a.g_log2, acc, arg);
+  acc.combine_slots(a.g_log2);
 
   if (a.counts && tile == 0 && ((heavy && threadIdx.x == 0) || (!heavy && lane == 0)))
     a.counts[row] = deg;
 
   if (!heavy) {
-    if (slot == 0) write_row<T, RHO, V, P>(a, row, deg, colv, valid, acc, arg);
+    if (slot == 0) write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
     return;
   }
   // CTA mode: merge the warp partials in warp order through shared memory.
   if (slot == 0) {
 #pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const int cl = (gl + G * p) * V + k;
-        s_acc[warp][cl] = acc[p][k];
-        if constexpr (RHO != RHO_SUM) s_arg[warp][cl] = arg[p][k];
+    for (int k = 0; k < V; ++k) {
+      const int cl = gl * V + k;
+      if constexpr (RHO == RHO_SUM) {
+        s_acc[warp][cl] = acc.acc[k];
+      } else {
+        s_cur[warp][cl] = acc.cur[k];
+        s_arg[warp][cl] = acc.arg[k];
       }
+    }
   }
   __syncthreads();
   if (warp == 0 && slot == 0) {
 #pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const int cl = (gl + G * p) * V + k;
+    for (int k = 0; k < V; ++k) {
+      const int cl = gl * V + k;
+      if constexpr (RHO == RHO_SUM) {
         double v = s_acc[0][cl];
-        int32_t ar = 0x7fffffff;
-        if constexpr (RHO != RHO_SUM) ar = s_arg[0][cl];
-        for (int w = 1; w < kWarpsPerCta; ++w) {
-          if constexpr (RHO == RHO_SUM) v += s_acc[w][cl];
-          else ext_update<RHO>(v, ar, s_acc[w][cl], s_arg[w][cl]);
-        }
-        acc[p][k] = v;
-        arg[p][k] = ar;
+        for (int w = 1; w < kWarpsPerCta; ++w) v += s_acc[w][cl];
+        acc.acc[k] = v;
+      } else {
+        acc.cur[k] = s_cur[0][cl];
+        acc.arg[k] = s_arg[0][cl];
+        for (int w = 1; w < kWarpsPerCta; ++w) acc.merge(k, 0.0, s_cur[w][cl], s_arg[w][cl]);
       }
-    write_row<T, RHO, V, P>(a, row, deg, colv, valid, acc, arg);
+    }
+    write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
   }
 }
 
-template <typename T, int OP, int RHO, int V, int P>
+template <typename T, int OP, int RHO, int V, int MP>
 cudaError_t launch_spmm_rows_t(const SpmmArgs& a, int64_t grid, cudaStream_t s) {
-  spmm_rows_kernel<T, OP, RHO, V, P><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
+  spmm_rows_kernel<T, OP, RHO, V, MP><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 
+// float: hot mode pairs get their own kernels; double (the parity
+// instantiation) always uses the run-time-mode kernel.
 template <typename T, int OP, int RHO, int V>
-cudaError_t launch_spmm_rows_p(int P, const SpmmArgs& a, int64_t grid, cudaStream_t s) {
-  if (P == 1) return launch_spmm_rows_t<T, OP, RHO, V, 1>(a, grid, s);
-  return launch_spmm_rows_t<T, OP, RHO, V, 2>(a, grid, s);
+cudaError_t launch_spmm_rows_mp(int mp, const SpmmArgs& a, int64_t grid, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {
+    if constexpr (OP == OP_COPY) {
+      if (mp == MP_F) return launch_spmm_rows_t<T, OP, RHO, V, MP_F>(a, grid, s);
+    } else if constexpr (OP != OP_DIV) {
+      if (mp == MP_FF) return launch_spmm_rows_t<T, OP, RHO, V, MP_FF>(a, grid, s);
+      if (mp == MP_FS) return launch_spmm_rows_t<T, OP, RHO, V, MP_FS>(a, grid, s);
+      if (mp == MP_FH) return launch_spmm_rows_t<T, OP, RHO, V, MP_FH>(a, grid, s);
+    }
+  }
+  return launch_spmm_rows_t<T, OP, RHO, V, MP_GEN>(a, grid, s);
 }
 
 template <typename T, int OP, int RHO>
-cudaError_t launch_spmm_rows_v(int V, int P, const SpmmArgs& a, int64_t grid, cudaStream_t s) {
+cudaError_t launch_spmm_rows_v(int V, int mp, const SpmmArgs& a, int64_t grid, cudaStream_t s) {
   if constexpr (sizeof(T) == 4) {
-    if (V == 4) return launch_spmm_rows_p<T, OP, RHO, 4>(P, a, grid, s);
+    if (V == 4) return launch_spmm_rows_mp<T, OP, RHO, 4>(mp, a, grid, s);
   }
-  if (V == 2) return launch_spmm_rows_p<T, OP, RHO, 2>(P, a, grid, s);
-  return launch_spmm_rows_p<T, OP, RHO, 1>(P, a, grid, s);
+  if (V == 2) return launch_spmm_rows_mp<T, OP, RHO, 2>(mp, a, grid, s);
+  return launch_spmm_rows_mp<T, OP, RHO, 1>(mp, a, grid, s);
 }
 
 // Instantiated once per OP in spmm_op_<op>.cu so the op families compile in
 // parallel.
 template <int OP>
-cudaError_t launch_spmm_rows(int dtype_is_f64, int rho, int V, int P, const SpmmArgs& a,
+cudaError_t launch_spmm_rows(int dtype_is_f64, int rho, int V, int mp, const SpmmArgs& a,
                              int64_t grid, cudaStream_t s) {
   if (dtype_is_f64) {
-    if (rho == RHO_SUM) return launch_spmm_rows_v<double, OP, RHO_SUM>(V, P, a, grid, s);
-    if (rho == RHO_MAX) return launch_spmm_rows_v<double, OP, RHO_MAX>(V, P, a, grid, s);
-    return launch_spmm_rows_v<double, OP, RHO_MIN>(V, P, a, grid, s);
+    if (rho == RHO_SUM) return launch_spmm_rows_v<double, OP, RHO_SUM>(V, mp, a, grid, s);
+    if (rho == RHO_MAX) return launch_spmm_rows_v<double, OP, RHO_MAX>(V, mp, a, grid, s);
+    return launch_spmm_rows_v<double, OP, RHO_MIN>(V, mp, a, grid, s);
   }
-  if (rho == RHO_SUM) return launch_spmm_rows_v<float, OP, RHO_SUM>(V, P, a, grid, s);
-  if (rho == RHO_MAX) return launch_spmm_rows_v<float, OP, RHO_MAX>(V, P, a, grid, s);
-  return launch_spmm_rows_v<float, OP, RHO_MIN>(V, P, a, grid, s);
+  if (rho == RHO_SUM) return launch_spmm_rows_v<float, OP, RHO_SUM>(V, mp, a, grid, s);
+  if (rho == RHO_MAX) return launch_spmm_rows_v<float, OP, RHO_MAX>(V, mp, a, grid, s);
+  return launch_spmm_rows_v<float, OP, RHO_MIN>(V, mp, a, grid, s);
 }
 
 }  // namespace gmp
