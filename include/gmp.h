@@ -36,8 +36,10 @@ enum { GMP_OK = 0, GMP_EINVAL = 1, GMP_ECUDA = 2, GMP_EUNSUPPORTED = 3 };
 /* message ops: kernels.py:43 OPS ("copy_lhs","copy_rhs","add","sub","mul","div","dot") */
 enum { GMP_COPY_LHS = 0, GMP_COPY_RHS = 1, GMP_ADD = 2, GMP_SUB = 3,
        GMP_MUL = 4, GMP_DIV = 5, GMP_DOT = 6 };
-/* operand targets: kernels.py:44 TARGETS ("src","dst","edge"); NONE for copy's unused side */
-enum { GMP_NONE = -1, GMP_SRC = 0, GMP_DST = 1, GMP_EDGE = 2 };
+/* operand targets: kernels.py:44 TARGETS ("src","dst","edge"); NONE for copy's unused side.
+ * GMP_EDGE_POS is an edge operand already permuted into the adjacency's order
+ * (row p holds edge eids[p]; see gmp_gather_rows) - g-SpMM only. */
+enum { GMP_NONE = -1, GMP_SRC = 0, GMP_DST = 1, GMP_EDGE = 2, GMP_EDGE_POS = 3 };
 /* reducers: kernels.py:45 REDUCERS ("sum","max","min","mean") */
 enum { GMP_SUM = 0, GMP_MAX = 1, GMP_MIN = 2, GMP_MEAN = 3 };
 /* feature dtypes */
@@ -140,19 +142,27 @@ int gmp_gsddmm(const gmp_coo* coo, int op, int dtype,
 
 /* ---- edge_softmax ---------------------------------------------------------
  * Replaces messaging.edge_softmax (messaging.py:105-126: gspmm max, gsddmm
- * sub, exp, gspmm sum, gsddmm div) with ONE fused per-destination pass:
+ * sub, exp, gspmm sum, gsddmm div) with two fused kernels: a per-destination
+ * statistics pass over the in-adjacency (max and sum of exp per head) and an
+ * edge-parallel pass over the COO list writing
  *   alpha[e,h] = exp(s[e,h] - max_{e'->v} s[e',h]) / sum_{e'->v} exp(...)
- * scores/alpha: (m, H) row-major keyed by edge id, leading dims lds/lda. */
-int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
-                         const void* scores, int64_t lds, int32_t H,
-                         void* alpha, int64_t lda, void* stream);
+ * scores/alpha: (m, H) row-major keyed by edge id, leading dims lds/lda.
+ * workspace: gmp_edge_softmax_workspace_size(n_rows, H) bytes of device
+ * memory for the per-destination statistics. */
+size_t gmp_edge_softmax_workspace_size(int64_t n_rows, int32_t H);
+
+int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sched* sched,
+                         int dtype, const void* scores, int64_t lds, int32_t H,
+                         void* alpha, int64_t lda, void* workspace, size_t workspace_bytes,
+                         void* stream);
 
 /* Fused backward of edge_softmax (the composition of the four kernel
  * backwards of messaging.py:117-121, autodiff.py:398-418):
  *   ds[e,h] = alpha[e,h] * (g[e,h] - sum_{e'->v} alpha[e',h] g[e',h]) */
-int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
-                         const void* alpha, int64_t lda, const void* grad, int64_t ldg,
-                         int32_t H, void* ds, int64_t ldds, void* stream);
+int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sched* sched,
+                         int dtype, const void* alpha, int64_t lda, const void* grad,
+                         int64_t ldg, int32_t H, void* ds, int64_t ldds, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* ---- extrema gradient routing ----------------------------------------------
  * Replaces kernels.route_extrema_grad (kernels.py:843-857): dM[arg[v,k], k] =
@@ -170,6 +180,13 @@ int gmp_route_extrema(int64_t n_rows, int32_t d, int dtype, const int64_t* arg,
 int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* arg,
                          const void* dZ, int64_t lddz, const int32_t* target_index,
                          void* dOut, int64_t ldo, void* stream);
+
+/* ---- row gather ------------------------------------------------------------
+ * dst[i, :] = src[idx[i], :] for i < n (dim columns). Used to lay an edge
+ * operand out in adjacency order once (idx = the adjacency's eids) so that a
+ * multi-tile g-SpMM reads it coalesced instead of gathering it per tile. */
+int gmp_gather_rows(int64_t n, int32_t dim, int dtype, const int32_t* idx, const void* src,
+                    int64_t lds, void* dst, int64_t ldd, void* stream);
 
 /* ---- diagnostics ------------------------------------------------------------ */
 const char* gmp_last_error(void);

@@ -15,13 +15,13 @@ LIB_PATH = Path(__file__).resolve().parent / "libgmp.so"
 # enums (include/gmp.h)
 GMP_OK, GMP_EINVAL, GMP_ECUDA, GMP_EUNSUPPORTED = 0, 1, 2, 3
 OPS = {"copy_lhs": 0, "copy_rhs": 1, "add": 2, "sub": 3, "mul": 4, "div": 5, "dot": 6}
-TARGETS = {None: -1, "src": 0, "dst": 1, "edge": 2}
+TARGETS = {None: -1, "src": 0, "dst": 1, "edge": 2, "edge_pos": 3}
 RHOS = {"sum": 0, "max": 1, "min": 2, "mean": 3}
 GMP_F32, GMP_F64 = 0, 1
 
 EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "gmp_gsddmm",
-            "gmp_edge_softmax_fwd", "gmp_edge_softmax_bwd", "gmp_route_extrema",
-            "gmp_extrema_bwd_copy", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
+            "gmp_edge_softmax_workspace_size", "gmp_edge_softmax_fwd", "gmp_edge_softmax_bwd", "gmp_route_extrema",
+            "gmp_extrema_bwd_copy", "gmp_gather_rows", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
             "gmp_version")
 
 
@@ -71,18 +71,22 @@ def _declare(lib):
                               _P(GmpTuning), vp]
     lib.gmp_gsddmm.argtypes = [_P(GmpCoo), c_int, c_int, _P(GmpOperand), _P(GmpOperand),
                                vp, i64, i32, vp, vp]
-    lib.gmp_edge_softmax_fwd.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, vp, i64, i32, vp, i64, vp]
-    lib.gmp_edge_softmax_bwd.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, vp, i64, vp, i64, i32,
-                                         vp, i64, vp]
+    lib.gmp_edge_softmax_workspace_size.argtypes = [i64, i32]
+    lib.gmp_edge_softmax_workspace_size.restype = ctypes.c_size_t
+    lib.gmp_edge_softmax_fwd.argtypes = [_P(GmpAdj), _P(GmpCoo), _P(GmpSched), c_int, vp, i64, i32,
+                                         vp, i64, vp, ctypes.c_size_t, vp]
+    lib.gmp_edge_softmax_bwd.argtypes = [_P(GmpAdj), _P(GmpCoo), _P(GmpSched), c_int, vp, i64, vp,
+                                         i64, i32, vp, i64, vp, ctypes.c_size_t, vp]
     lib.gmp_route_extrema.argtypes = [i64, i32, c_int, vp, vp, i64, vp, i64, vp]
     lib.gmp_extrema_bwd_copy.argtypes = [i64, i32, c_int, vp, vp, i64, vp, vp, i64, vp]
+    lib.gmp_gather_rows.argtypes = [i64, i32, c_int, vp, vp, i64, vp, i64, vp]
     lib.gmp_last_error.restype = ctypes.c_char_p
     lib.gmp_strerror.argtypes = [c_int]
     lib.gmp_strerror.restype = ctypes.c_char_p
     lib.gmp_launch_count.restype = ctypes.c_uint64
     for name in ("gmp_build_schedule", "gmp_gspmm", "gmp_gsddmm", "gmp_edge_softmax_fwd",
                  "gmp_edge_softmax_bwd", "gmp_route_extrema", "gmp_extrema_bwd_copy",
-                 "gmp_version"):
+                 "gmp_gather_rows", "gmp_version"):
         getattr(lib, name).restype = c_int
 
 

@@ -24,6 +24,8 @@ cudaError_t launch_route_extrema(int, int64_t, int32_t, const int64_t*, const vo
 cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const void*, int64_t,
                                     const int32_t*, void*, int64_t, cudaStream_t);
 size_t schedule_workspace_bytes(int64_t n);
+cudaError_t launch_gather_rows(int, int64_t, int32_t, const int32_t*, const void*, int64_t, void*,
+                               int64_t, cudaStream_t);
 cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t* order_out,
                            void* ws, size_t ws_bytes, int64_t* n_heavy, int64_t* n_nonempty,
                            cudaStream_t s);
@@ -112,7 +114,7 @@ int check_operands(int op, const gmp_operand* lhs, const gmp_operand* rhs, int32
   const bool binary = op >= GMP_ADD;
   const gmp_operand* used = (op == GMP_COPY_RHS) ? rhs : lhs;
   if (!used || !used->data) return fail(GMP_EINVAL, "phi %s needs its operand", op_name(op));
-  if (used->target < GMP_SRC || used->target > GMP_EDGE)
+  if (used->target < GMP_SRC || used->target > GMP_EDGE_POS)
     return fail(GMP_EINVAL, "bad operand target %d", used->target);
   if (used->dim < 0 || used->ld < used->dim) return fail(GMP_EINVAL, "bad operand dim/ld");
   if (!binary) {
@@ -120,7 +122,7 @@ int check_operands(int op, const gmp_operand* lhs, const gmp_operand* rhs, int32
     return GMP_OK;
   }
   if (!rhs || !rhs->data) return fail(GMP_EINVAL, "phi %s needs its rhs operand", op_name(op));
-  if (rhs->target < GMP_SRC || rhs->target > GMP_EDGE)
+  if (rhs->target < GMP_SRC || rhs->target > GMP_EDGE_POS)
     return fail(GMP_EINVAL, "bad operand target %d", rhs->target);
   if (lhs->target == rhs->target) return fail(GMP_EINVAL, "binary op targets must differ");
   if (rhs->dim < 0 || rhs->ld < rhs->dim) return fail(GMP_EINVAL, "bad operand dim/ld");
@@ -183,6 +185,7 @@ RowOperand row_operand(const Opnd& o) {
   r.data = o.dev.data;
   r.ld = (uint32_t)o.dev.ld;
   r.from_eid = o.dev.target == GMP_EDGE;
+  r.from_pos = o.dev.target == GMP_EDGE_POS;
   r.bcast = o.dev.bcast;
   r.mode = o.dev.target == GMP_DST ? M_HOIST : (o.dev.bcast ? M_SCALAR : M_FULL);
   return r;
@@ -270,6 +273,8 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
   cudaError_t e;
 
   if (kop == OP_DOT) {
+    if (L->target == GMP_EDGE_POS || (R && R->target == GMP_EDGE_POS))
+      return fail(GMP_EINVAL, "dot messages take edge operands in edge-id order");
     const int dim = L->dim;
     SpmmDotArgs a{};
     a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
@@ -337,6 +342,8 @@ int gmp_gsddmm(const gmp_coo* coo, int op, int dtype, const gmp_operand* lhs, co
   if (d_out != want) return fail(GMP_EINVAL, "d_out %d does not match phi's output width %d", d_out, want);
   if (ldm < d_out || (!M && coo->m > 0 && d_out > 0)) return fail(GMP_EINVAL, "bad output M/ldm");
   if (op == GMP_DIV && !err_eid) return fail(GMP_EINVAL, "div needs the err_eid slot");
+  if ((lhs && lhs->target == GMP_EDGE_POS) || (rhs && rhs->target == GMP_EDGE_POS))
+    return fail(GMP_EINVAL, "GMP_EDGE_POS operands are g-SpMM only");
   if (coo->m == 0 || d_out == 0) return GMP_OK;
   if (!coo->src || !coo->dst) return fail(GMP_EINVAL, "null coo arrays");
   const size_t F = dtype == GMP_F64 ? 8 : 4;
@@ -365,15 +372,24 @@ int gmp_gsddmm(const gmp_coo* coo, int op, int dtype, const gmp_operand* lhs, co
   return cuda_status(e, "gmp_gsddmm");
 }
 
-static int softmax_common(const gmp_adj* adj, const gmp_sched* sched, int dtype, const void* s,
-                          int64_t lds, const void* g, int64_t ldg, int32_t H, void* out,
-                          int64_t ldo, bool bwd, void* stream) {
-  if (!adj) return fail(GMP_EINVAL, "null adjacency");
+size_t gmp_edge_softmax_workspace_size(int64_t n_rows, int32_t H) {
+  return (size_t)std::max<int64_t>(0, n_rows) * (size_t)std::max(0, H) * 2 * sizeof(double);
+}
+
+static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sched* sched,
+                          int dtype, const void* s, int64_t lds, const void* g, int64_t ldg,
+                          int32_t H, void* out, int64_t ldo, void* ws, size_t ws_bytes, bool bwd,
+                          void* stream) {
+  if (!adj || !coo) return fail(GMP_EINVAL, "null adjacency or coo");
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
   if (adj->m < 0 || adj->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
+  if (coo->m != adj->m) return fail(GMP_EINVAL, "coo and adjacency edge counts differ");
   if (H < 0 || lds < H || ldo < H || (bwd && ldg < H)) return fail(GMP_EINVAL, "bad head count / ld");
   if (adj->m == 0 || H == 0 || adj->n_rows == 0) return GMP_OK;
-  if (!s || !out || (bwd && !g) || !adj->eids || !adj->indptr) return fail(GMP_EINVAL, "null arrays");
+  if (!s || !out || (bwd && !g) || !adj->eids || !adj->indptr || !coo->dst)
+    return fail(GMP_EINVAL, "null arrays");
+  if (!ws || ws_bytes < gmp_edge_softmax_workspace_size(adj->n_rows, H))
+    return fail(GMP_EINVAL, "softmax workspace too small");
   const size_t F = dtype == GMP_F64 ? 8 : 4;
   Opnd ops[2] = {};
   ops[0].present = true; ops[0].dev.data = s; ops[0].dev.ld = lds;
@@ -390,22 +406,43 @@ static int softmax_common(const gmp_adj* adj, const gmp_sched* sched, int dtype,
   a.blocks_per_tile = n_heavy + (adj->n_rows - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
   a.H = H; a.tile_cols = tw; a.g_log2 = log2i(G);
   a.s = s; a.lds = lds; a.g = g; a.ldg = ldg; a.out = out; a.ldo = ldo;
-  cudaError_t e = launch_edge_softmax(F == 8, V, bwd, a, a.blocks_per_tile * ntiles,
-                                      (cudaStream_t)stream);
+  a.dst = coo->dst; a.m = coo->m;
+  a.stat = ws;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = launch_edge_softmax(F == 8, V, bwd, a, a.blocks_per_tile * ntiles, st);
   g_launches++;
+  if (e == cudaSuccess) {
+    e = launch_edge_softmax_apply(F == 8, V, bwd, a, st);
+    g_launches++;
+  }
   return cuda_status(e, bwd ? "gmp_edge_softmax_bwd" : "gmp_edge_softmax_fwd");
 }
 
-int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
-                         const void* scores, int64_t lds, int32_t H, void* alpha, int64_t lda,
-                         void* stream) {
-  return softmax_common(in_adj, sched, dtype, scores, lds, nullptr, 0, H, alpha, lda, false, stream);
+int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sched* sched,
+                         int dtype, const void* scores, int64_t lds, int32_t H, void* alpha,
+                         int64_t lda, void* workspace, size_t workspace_bytes, void* stream) {
+  return softmax_common(in_adj, coo, sched, dtype, scores, lds, nullptr, 0, H, alpha, lda,
+                        workspace, workspace_bytes, false, stream);
 }
 
-int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
-                         const void* alpha, int64_t lda, const void* grad, int64_t ldg, int32_t H,
-                         void* ds, int64_t ldds, void* stream) {
-  return softmax_common(in_adj, sched, dtype, alpha, lda, grad, ldg, H, ds, ldds, true, stream);
+int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sched* sched,
+                         int dtype, const void* alpha, int64_t lda, const void* grad, int64_t ldg,
+                         int32_t H, void* ds, int64_t ldds, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  return softmax_common(in_adj, coo, sched, dtype, alpha, lda, grad, ldg, H, ds, ldds, workspace,
+                        workspace_bytes, true, stream);
+}
+
+int gmp_gather_rows(int64_t n, int32_t dim, int dtype, const int32_t* idx, const void* src,
+                    int64_t lds, void* dst, int64_t ldd, void* stream) {
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (n < 0 || dim < 0 || lds < dim || ldd < dim) return fail(GMP_EINVAL, "bad sizes");
+  if (n == 0 || dim == 0) return GMP_OK;
+  if (!idx || !src || !dst) return fail(GMP_EINVAL, "null arrays");
+  cudaError_t e = launch_gather_rows(dtype == GMP_F64, n, dim, idx, src, lds, dst, ldd,
+                                     (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_gather_rows");
 }
 
 int gmp_route_extrema(int64_t n_rows, int32_t d, int dtype, const int64_t* arg, const void* dZ,

@@ -88,6 +88,15 @@ __device__ __forceinline__ double apply_op(double a, double b) {
   else return a;                                  // OP_COPY
 }
 
+template <int OP, typename T>
+__device__ __forceinline__ T apply_op_t(T a, T b) {
+  if constexpr (OP == OP_ADD) return a + b;
+  else if constexpr (OP == OP_SUB) return a - b;
+  else if constexpr (OP == OP_MUL) return a * b;
+  else if constexpr (OP == OP_DIV) return a / b;
+  else return a;
+}
+
 // ---- extrema combine: strictly better value wins; ties keep the smaller edge
 // id (kernels.py:402-408 masked min-reduce over edge ids).
 template <int RHO>

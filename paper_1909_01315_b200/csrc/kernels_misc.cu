@@ -82,6 +82,29 @@ cudaError_t launch_edge_softmax(int f64, int V, bool bwd, const SoftmaxArgs& a, 
   return cudaGetLastError();
 }
 
+template <typename T, bool BWD>
+static void softmax_apply_v(int V, const SoftmaxArgs& a, cudaStream_t s) {
+  const int64_t total = a.m * (int64_t)(a.H / V);
+  const unsigned grid = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((total + 256 * kApplyU - 1) / (256 * kApplyU), 148 * 64));
+  if constexpr (sizeof(T) == 4) {
+    if (V == 4) { edge_softmax_apply_kernel<T, 4, BWD><<<grid, 256, 0, s>>>(a); return; }
+  }
+  if (V == 2) { edge_softmax_apply_kernel<T, 2, BWD><<<grid, 256, 0, s>>>(a); return; }
+  edge_softmax_apply_kernel<T, 1, BWD><<<grid, 256, 0, s>>>(a);
+}
+
+cudaError_t launch_edge_softmax_apply(int f64, int V, bool bwd, const SoftmaxArgs& a, cudaStream_t s) {
+  if (f64) {
+    if (bwd) softmax_apply_v<double, true>(V, a, s);
+    else softmax_apply_v<double, false>(V, a, s);
+  } else {
+    if (bwd) softmax_apply_v<float, true>(V, a, s);
+    else softmax_apply_v<float, false>(V, a, s);
+  }
+  return cudaGetLastError();
+}
+
 // ---- extrema gradient routing (kernels.py:843-857) --------------------------
 
 template <typename T>
@@ -132,6 +155,29 @@ cudaError_t launch_extrema_bwd_copy(int f64, int64_t n, int32_t d, const int64_t
   if (total == 0) return cudaSuccess;
   if (f64) extrema_bwd_copy_kernel<double><<<grid, 256, 0, s>>>(n, d, arg, (const double*)dZ, lddz, tindex, (double*)dOut, ldo);
   else extrema_bwd_copy_kernel<float><<<grid, 256, 0, s>>>(n, d, arg, (const float*)dZ, lddz, tindex, (float*)dOut, ldo);
+  return cudaGetLastError();
+}
+
+// ---- row gather: dst[i] = src[idx[i]] ------------------------------------------
+
+template <typename T>
+__global__ void gather_rows_kernel(int64_t n, int32_t dim, const int32_t* __restrict__ idx,
+                                   const T* __restrict__ src, int64_t lds, T* dst, int64_t ldd) {
+  const int64_t total = n * (int64_t)dim;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / dim;
+    const int c = (int)(i - r * dim);
+    dst[r * ldd + c] = __ldg(src + (int64_t)__ldg(idx + r) * lds + c);
+  }
+}
+
+cudaError_t launch_gather_rows(int f64, int64_t n, int32_t dim, const int32_t* idx, const void* src,
+                               int64_t lds, void* dst, int64_t ldd, cudaStream_t s) {
+  const int64_t total = n * (int64_t)dim;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  if (f64) gather_rows_kernel<double><<<grid, 256, 0, s>>>(n, dim, idx, (const double*)src, lds, (double*)dst, ldd);
+  else gather_rows_kernel<float><<<grid, 256, 0, s>>>(n, dim, idx, (const float*)src, lds, (float*)dst, ldd);
   return cudaGetLastError();
 }
 

@@ -9,6 +9,7 @@
 #pragma once
 
 #include "gmp_common.cuh"
+#include "softmax.cuh"
 
 namespace gmp {
 
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(256) sddmm_kernel(const SddmmArgs a) {
       const int32_t v = __shfl_sync(kFull, sv, j & 31);
       const int64_t e = b + j;
       if constexpr (OP == OP_DOT) {
-        double s = 0.0;
+        ColSum<T> cs;
         if (j < cnt) {
           const T* pa = static_cast<const T*>(a.lhs.data) + operand_row(a.lhs, u, v, e) * a.lhs.ld;
           const T* pb = static_cast<const T*>(a.rhs.data) + operand_row(a.rhs, u, v, e) * a.rhs.ld;
@@ -71,9 +72,10 @@ __global__ void __launch_bounds__(256) sddmm_kernel(const SddmmArgs a) {
             load_vec<T, V>(pa + c, xa);
             load_vec<T, V>(pb + c, xb);
 #pragma unroll
-            for (int k = 0; k < V; ++k) s += (double)xa[k] * (double)xb[k];
+            for (int k = 0; k < V; ++k) cs.add_prod(xa[k], xb[k]);
           }
         }
+        double s = cs.value();
         for (int off = 1; off < G; off <<= 1) s += shfl_xor_d(s, off);
         if (j < cnt && gl == 0) static_cast<T*>(a.M)[e * a.ldm] = (T)s;
       } else {
@@ -89,7 +91,10 @@ __global__ void __launch_bounds__(256) sddmm_kernel(const SddmmArgs a) {
 #pragma unroll
           for (int k = 0; k < V; ++k) {
             if constexpr (OP == OP_DIV) zero |= (xb[k] == T(0));
-            r[k] = (T)apply_op<OP>((double)xa[k], BIN ? (double)xb[k] : 0.0);
+            // an IEEE op on T operands == the fp64 op rounded to T (no double
+            // rounding issue for + - * /), so the reference's fp64 message
+            // cast to T is reproduced bit-exactly without conversions
+            r[k] = apply_op_t<OP, T>(xa[k], BIN ? xb[k] : T(0));
           }
           store_vec<T, V>(out + c, r);
         }

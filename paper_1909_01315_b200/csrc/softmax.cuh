@@ -3,13 +3,25 @@
 // Forward replaces messaging.edge_softmax (messaging.py:105-126), which
 // dispatches gspmm(copy_rhs(edge), max) -> gsddmm(sub(edge,dst)) -> exp ->
 // gspmm(copy_rhs(edge), sum) -> gsddmm(div(edge,dst)) and keeps four (m,H) /
-// (n,H) temporaries. Here one kernel walks each destination's in-edges twice:
-//   pass 1: online (max, sum of exp) per head column, fp64 sum;
-//   pass 2: alpha = exp(s - max) / sum, written at the edge id.
+// (n,H) temporaries. Here two kernels do it:
+//   stats : walk each destination's in-edges once (CSC row schedule of
+//           spmm_rows.cuh: degree-sorted, CTA per heavy row, warp per light
+//           row) computing the online (max, sum of exp) per head column;
+//   apply : edge-parallel over the COO list in edge-id order - coalesced
+//           reads of s and writes of alpha = exp(s - max[dst]) / sum[dst].
+// Edge-keyed data is random in CSC order (one 32 B sector per edge, fetched
+// at 64 B granularity), so reading it once in row order and once streaming
+// beats two row-order passes, whose second pass misses L2 when many large
+// rows are in flight (measured: 7.2 ms -> see profiles/).
 // Backward (the composition of those four kernel backwards, autodiff.py:398-418)
-// is the closed form  ds = alpha * (g - sum_{in-edges} alpha * g), again two
-// passes per destination. Same row schedule as spmm_rows.cuh (degree-sorted,
-// CTA per heavy row, warp per light row); columns tiled when H > 32 * V.
+// is the closed form  ds = alpha * (g - sum_{in-edges} alpha * g): the stats
+// kernel computes the per-destination sums, the apply kernel the edges.
+//
+// Numerics: fp32 sums use the exact compensated pair of spmm_rows.cuh (no
+// per-element fp32->fp64 conversions, which run on the XU pipe) and are
+// folded to fp64 once per row; the backward's g - sum is formed with a
+// two-float representation of the fp64 sum. The fp64 instantiation computes
+// everything in double.
 #pragma once
 
 #include "gmp_common.cuh"
@@ -33,24 +45,57 @@ struct SoftmaxArgs {
   int64_t ldg;
   void* out;       // alpha (fwd) / ds (bwd)
   int64_t ldo;
+  const int32_t* dst;  // COO destinations (apply kernel)
+  int64_t m;
+  void* stat;          // (n_rows, 2H) of T: [max | 1/sum] fwd, [sum_hi | sum_lo] bwd
 };
 
 __device__ __forceinline__ float exp_t(float x) { return expf(x); }
 __device__ __forceinline__ double exp_t(double x) { return exp(x); }
 
-// (m, l) online-softmax merge; empty partials carry m = -inf, l = 0.
+// (m, l) online-softmax merge in fp64 for l; empty partials carry m = -inf.
 template <typename T>
 __device__ __forceinline__ void sm_merge(T& m, double& l, T om, double ol) {
   if (om == -INFINITY) return;
   if (m == -INFINITY) { m = om; l = ol; return; }
-  if (om > m) { l = l * (double)exp_t(T(m - om)) + ol; m = om; }
-  else        { l += ol * (double)exp_t(T(om - m)); }
+  if (om > m) { l = l * exp((double)m - (double)om) + ol; m = om; }
+  else        { l += ol * exp((double)om - (double)m); }
 }
+
+// per-column running sum: compensated fp32 pair for float, plain fp64 for double
+template <typename T> struct ColSum;
+template <> struct ColSum<float> {
+  float s = 0.f, c = 0.f;
+  __device__ __forceinline__ void add(float x) { two_sum1(s, c, x); }
+  __device__ __forceinline__ void add_prod(float x, float y) {
+    const float p = __fmul_rn(x, y);
+    two_sum1(s, c, p);
+    c = __fadd_rn(c, __fmaf_rn(x, y, -p));
+  }
+  __device__ __forceinline__ void scale(float f) { s = __fmul_rn(s, f); c = __fmul_rn(c, f); }
+  __device__ __forceinline__ double value() const { return (double)s + (double)c; }
+};
+template <> struct ColSum<double> {
+  double s = 0.0;
+  __device__ __forceinline__ void add(double x) { s += x; }
+  __device__ __forceinline__ void add_prod(double x, double y) { s += x * y; }
+  __device__ __forceinline__ void scale(double f) { s *= f; }
+  __device__ __forceinline__ double value() const { return s; }
+};
+
+// Stats kernel: edges of a row are walked in chunks of kChunk whose edge ids
+// are staged in shared memory (coalesced loads, one chunk ahead), so every
+// lane keeps U independent score loads in flight even when 32 edges fit in
+// one warp step.
+constexpr int kChunk = 256;
 
 template <typename T, int V, bool BWD>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const SoftmaxArgs a) {
+  constexpr int U = V == 4 ? 4 : 8;
+  constexpr int B = kChunk / 32;
   __shared__ double s_l[kWarpsPerCta][32 * V];
   __shared__ T s_m[kWarpsPerCta][32 * V];
+  __shared__ int32_t s_eid[kWarpsPerCta][kChunk];
   const int64_t bid = blockIdx.x;
   const int tile = (int)(bid / a.blocks_per_tile);
   const int64_t local = bid - (int64_t)tile * a.blocks_per_tile;
@@ -68,48 +113,83 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
     row = a.order ? (int64_t)a.order[r] : r;
   }
   const int64_t pb = a.indptr[row], pe = a.indptr[row + 1];
-  if (pe == pb) return;  // no in-edges: nothing keyed to this row (block-uniform when heavy)
+  if (pe == pb) return;  // no in-edges: nothing keyed to this row (heavy rows are never empty)
   const int col = c0 + gl * V;
   const bool valid = col < c1;
-  const T* S = static_cast<const T*>(a.s);
-  const T* Gd = static_cast<const T*>(a.g);
-  T* O = static_cast<T*>(a.out);
-  const int64_t first = heavy ? (int64_t)warp * 32 : 0;
-  const int64_t stride = heavy ? 32 * kWarpsPerCta : 32;
+  const int ccol = valid ? col : 0;
+  const T* S = static_cast<const T*>(a.s) + ccol;
+  const T* Gd = static_cast<const T*>(a.g) + ccol;
+  T* O = static_cast<T*>(a.out) + ccol;
+  const int64_t first = heavy ? (int64_t)warp * kChunk : 0;
+  const int64_t stride = heavy ? (int64_t)kChunk * kWarpsPerCta : kChunk;
+  int32_t* buf = s_eid[warp];
 
-  // ---- pass 1 ----
+  // stage chunk `cb` of edge ids into this warp's buffer (prefetched registers)
+  int32_t pre[B];
+  auto fetch = [&](int64_t cb) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const int64_t q = cb + i * 32 + lane;
+      pre[i] = q < pe ? __ldg(a.eids + q) : 0;
+    }
+  };
+  auto stage = [&]() {
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < B; ++i) buf[i * 32 + lane] = pre[i];
+    __syncwarp();
+  };
+
+  // ---- pass 1: online max + sum (fwd) / sum of alpha * g (bwd) ----
   T m[V];
-  double l[V];
+  ColSum<T> acc[V];
 #pragma unroll
-  for (int k = 0; k < V; ++k) { m[k] = -INFINITY; l[k] = 0.0; }
-  for (int64_t base = pb + first; base < pe; base += stride) {
-    const int cnt = batch_count(pe - base);
-    const int32_t eb = lane < cnt ? __ldg(a.eids + base + lane) : 0;
-    for (int t = 0; t < cnt; t += E) {
-      const int j = t + slot;
-      const int32_t e = __shfl_sync(kFull, eb, j & 31);
-      if (j < cnt && valid) {
-        T x[V];
-        load_vec<T, V>(S + (int64_t)e * a.lds + col, x);
-        if constexpr (BWD) {
-          T gg[V];
-          load_vec<T, V>(Gd + (int64_t)e * a.ldg + col, gg);
+  for (int k = 0; k < V; ++k) m[k] = -INFINITY;
+  fetch(pb + first);
+  for (int64_t cb = pb + first; cb < pe; cb += stride) {
+    const int cnt = (int)min((int64_t)kChunk, pe - cb);
+    stage();
+    fetch(cb + stride);
+    for (int t = 0; t < cnt; t += E * U) {
+      T x[U][V], gg[U][V];
+      bool ok[U];
 #pragma unroll
-          for (int k = 0; k < V; ++k) l[k] += (double)x[k] * (double)gg[k];
-        } else {
+      for (int u = 0; u < U; ++u) {
+        const int j = t + slot + E * u;
+        ok[u] = j < cnt && valid;
+        const int64_t e = buf[j & (kChunk - 1)];
 #pragma unroll
-          for (int k = 0; k < V; ++k) {
-            if (x[k] > m[k]) { l[k] = l[k] * (double)exp_t(T(m[k] - x[k])) + 1.0; m[k] = x[k]; }
-            else             { l[k] += (double)exp_t(T(x[k] - m[k])); }
+        for (int k = 0; k < V; ++k) x[u][k] = gg[u][k] = T(0);
+        if (ok[u]) {
+          load_vec<T, V>(S + e * a.lds, x[u]);
+          if constexpr (BWD) load_vec<T, V>(Gd + e * a.ldg, gg[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          if constexpr (BWD) {
+            acc[k].add_prod(x[u][k], gg[u][k]);
+          } else {
+            if (x[u][k] > m[k]) {
+              acc[k].scale(exp_t(T(m[k] - x[u][k])));
+              m[k] = x[u][k];
+            }
+            acc[k].add(exp_t(T(x[u][k] - m[k])));
           }
         }
       }
     }
   }
+  double l[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) l[k] = acc[k].value();
   for (int off = G; off < 32; off <<= 1) {
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-      const double ol = shfl_xor_d(l[k], off);
+      const double ol = __shfl_xor_sync(kFull, l[k], off);
       if constexpr (BWD) {
         l[k] += ol;
       } else {
@@ -141,36 +221,93 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
 #pragma unroll
     for (int k = 0; k < V; ++k) { m[k] = s_m[0][gl * V + k]; l[k] = s_l[0][gl * V + k]; }
   }
+  // every slot of the warp needs its lane-group's final (m, l)
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    l[k] = __shfl_sync(kFull, l[k], gl);
+    m[k] = __shfl_sync(kFull, m[k], gl);
+  }
 
-  // ---- pass 2 ----
-  T inv[V];
+  // ---- per-destination statistics: (max, 1/sum) fwd, (sum_hi, sum_lo) bwd ----
+  if (slot == 0 && valid) {
+    T* st = static_cast<T*>(a.stat) + row * 2 * (int64_t)a.H + col;
 #pragma unroll
-  for (int k = 0; k < V; ++k) inv[k] = BWD ? T(0) : (T)(1.0 / l[k]);
-  for (int64_t base = pb + first; base < pe; base += stride) {
-    const int cnt = batch_count(pe - base);
-    const int32_t eb = lane < cnt ? __ldg(a.eids + base + lane) : 0;
-    for (int t = 0; t < cnt; t += E) {
-      const int j = t + slot;
-      const int32_t e = __shfl_sync(kFull, eb, j & 31);
-      if (j < cnt && valid) {
-        T x[V], r[V];
-        load_vec<T, V>(S + (int64_t)e * a.lds + col, x);
-        if constexpr (BWD) {
-          T gg[V];
-          load_vec<T, V>(Gd + (int64_t)e * a.ldg + col, gg);
-#pragma unroll
-          for (int k = 0; k < V; ++k) r[k] = (T)((double)x[k] * ((double)gg[k] - l[k]));
-        } else {
-#pragma unroll
-          for (int k = 0; k < V; ++k) r[k] = exp_t(T(x[k] - m[k])) * inv[k];
-        }
-        store_vec<T, V>(O + (int64_t)e * a.ldo + col, r);
+    for (int k = 0; k < V; ++k) {
+      if constexpr (BWD) {
+        const T hi = (T)l[k];
+        st[k] = hi;
+        st[a.H + k] = (T)(l[k] - (double)hi);
+      } else {
+        st[k] = m[k];
+        st[a.H + k] = (T)(1.0 / l[k]);
       }
+    }
+  }
+}
+
+// alpha[e] = exp(s[e] - max[dst e]) * inv_sum[dst e]   (fwd)
+// ds[e]    = alpha[e] * (g[e] - sum[dst e])            (bwd)
+// Edge-id order: s / g / alpha / ds stream coalesced; the per-destination
+// statistics (T pairs, (n, H)) are L2-resident gathers. Each thread keeps
+// kApplyU independent vectors in flight.
+constexpr int kApplyU = 4;
+
+template <typename T, int V, bool BWD>
+__global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxArgs a) {
+  const int per_edge = a.H / V;  // vectors per edge row
+  const int64_t total = a.m * (int64_t)per_edge;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const T* st = static_cast<const T*>(a.stat);
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < total;
+       i0 += nthreads * kApplyU) {
+    T x[kApplyU][V], gg[kApplyU][V], p0[kApplyU][V], p1[kApplyU][V];
+    int64_t ev[kApplyU];
+    int cv[kApplyU];
+    bool ok[kApplyU];
+#pragma unroll
+    for (int u = 0; u < kApplyU; ++u) {
+      const int64_t i = i0 + u * nthreads;
+      ok[u] = i < total;
+      const int64_t e = ok[u] ? i / per_edge : 0;
+      const int c = ok[u] ? (int)(i - e * per_edge) * V : 0;
+      ev[u] = e;
+      cv[u] = c;
+      const int64_t v = __ldg(a.dst + e);
+      load_vec<T, V>(static_cast<const T*>(a.s) + e * a.lds + c, x[u]);
+      if constexpr (BWD) load_vec<T, V>(static_cast<const T*>(a.g) + e * a.ldg + c, gg[u]);
+      // stats row v: [pair0 (H) | pair1 (H)] interleaved as 2*H per row
+      load_vec<T, V>(st + v * 2 * a.H + c, p0[u]);
+      load_vec<T, V>(st + v * 2 * a.H + a.H + c, p1[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kApplyU; ++u) {
+      if (!ok[u]) continue;
+      T r[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if constexpr (BWD) {
+          if constexpr (sizeof(T) == 8) {
+            r[k] = x[u][k] * (gg[u][k] - p0[u][k]);
+          } else {
+            // (g - l) to ~fp64 accuracy with l = lhi + llo (p0, p1)
+            float dh = 0.f, dc = 0.f;
+            two_sum1(dh, dc, (float)gg[u][k]);
+            two_sum1(dh, dc, -(float)p0[u][k]);
+            dc = __fsub_rn(dc, (float)p1[u][k]);
+            r[k] = (T)__fmaf_rn((float)x[u][k], dh, __fmul_rn((float)x[u][k], dc));
+          }
+        } else {
+          r[k] = exp_t(T(x[u][k] - p0[u][k])) * p1[u][k];
+        }
+      }
+      store_vec<T, V>(static_cast<T*>(a.out) + ev[u] * a.ldo + cv[u], r);
     }
   }
 }
 
 cudaError_t launch_edge_softmax(int dtype_is_f64, int V, bool bwd, const SoftmaxArgs& a,
                                 int64_t grid, cudaStream_t s);
+cudaError_t launch_edge_softmax_apply(int dtype_is_f64, int V, bool bwd, const SoftmaxArgs& a,
+                                      cudaStream_t s);
 
 }  // namespace gmp

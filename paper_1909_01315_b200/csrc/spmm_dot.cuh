@@ -8,6 +8,7 @@
 
 #include "gmp_common.cuh"
 #include "spmm_rows.cuh"
+#include "softmax.cuh"
 
 namespace gmp {
 
@@ -35,14 +36,15 @@ __device__ __forceinline__ double dot_partial(const OperandDev& a, const Operand
   const int64_t rb = b.target == T_SRC ? nbr : (b.target == T_DST ? row : eid);
   const T* pa = static_cast<const T*>(a.data) + ra * a.ld;
   const T* pb = static_cast<const T*>(b.data) + rb * b.ld;
-  double s = 0.0;
+  ColSum<T> cs;
   for (int c = gl * V; c < dim; c += G * V) {
     T xa[V], xb[V];
     load_vec<T, V>(pa + c, xa);
     load_vec<T, V>(pb + c, xb);
 #pragma unroll
-    for (int k = 0; k < V; ++k) s += (double)xa[k] * (double)xb[k];
+    for (int k = 0; k < V; ++k) cs.add_prod(xa[k], xb[k]);
   }
+  const double s = cs.value();
   return s;
 }
 

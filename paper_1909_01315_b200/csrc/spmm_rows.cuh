@@ -54,6 +54,7 @@ struct RowOperand {
   int32_t mode;      // M_FULL / M_SCALAR / M_HOIST
   int32_t from_eid;  // gathered by edge id (EDGE target) instead of neighbour id (SRC target)
   int32_t bcast;     // hoisted operand is a single column
+  int32_t from_pos;  // edge operand already permuted to adjacency order: row = position
 };
 
 struct SpmmArgs {
@@ -264,8 +265,6 @@ __device__ __forceinline__ void gather_full(const T* colbase, uint32_t ld_bytes,
   const T* p = reinterpret_cast<const T*>(reinterpret_cast<const char*>(colbase) +
                                           (uint64_t)(use ? row : 0u) * ld_bytes);
   load_vec<T, V>(p, out);
-#pragma unroll
-  for (int k = 0; k < V; ++k) out[k] = use ? out[k] : T(0);
 }
 
 // Accumulate the messages of edges [pb, pe) of one row owned by this warp:
@@ -304,10 +303,17 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
     nb1 = __ldg(indices + base + stride + lane);
     if (need_eid) eb1 = __ldg(eids + base + stride + lane);
   }
+  const bool l_pos = a.lhs.from_pos, r_pos = a.rhs.from_pos;
+  auto lrow = [&](int32_t nb, int32_t eb, int64_t at) -> uint32_t {
+    return l_pos ? (uint32_t)(at + lane) : (uint32_t)(l_eid ? eb : nb);
+  };
+  auto rrow = [&](int32_t nb, int32_t eb, int64_t at) -> uint32_t {
+    return r_pos ? (uint32_t)(at + lane) : (uint32_t)(r_eid ? eb : nb);
+  };
   T sa0 = T(0), sb0 = T(0);
   if (base + lane < pe) {
-    if (lm == M_SCALAR) sa0 = scalar_at<T>(a.lhs, l_eid ? eb0 : nb0);
-    if (rm == M_SCALAR) sb0 = scalar_at<T>(a.rhs, r_eid ? eb0 : nb0);
+    if (lm == M_SCALAR) sa0 = scalar_at<T>(a.lhs, lrow(nb0, eb0, base));
+    if (rm == M_SCALAR) sb0 = scalar_at<T>(a.rhs, rrow(nb0, eb0, base));
   }
   int since_fold = 0;
   for (; base < pe; base += stride) {
@@ -321,62 +327,72 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
     }
     T sa1 = T(0), sb1 = T(0);
     if (base + stride + lane < pe) {
-      if (lm == M_SCALAR) sa1 = scalar_at<T>(a.lhs, l_eid ? eb1 : nb1);
-      if (rm == M_SCALAR) sb1 = scalar_at<T>(a.rhs, r_eid ? eb1 : nb1);
+      if (lm == M_SCALAR) sa1 = scalar_at<T>(a.lhs, lrow(nb1, eb1, base + stride));
+      if (rm == M_SCALAR) sb1 = scalar_at<T>(a.rhs, rrow(nb1, eb1, base + stride));
     }
-    const uint32_t ra_lane = l_eid ? eb0 : nb0;
-    const uint32_t rb_lane = r_eid ? eb0 : nb0;
+    const uint32_t ra_lane = lrow(nb0, eb0, base);
+    const uint32_t rb_lane = rrow(nb0, eb0, base);
+    // One 32-edge batch. FULLB: all 32 edges present and E*U <= 32, so no
+    // edge masking at all (lanes with !valid columns accumulate junk that is
+    // never stored) - the common case inside heavy rows.
+    auto pass = [&](auto full_tag) {
+      constexpr bool FULLB = decltype(full_tag)::value;
 #pragma unroll 1
-    for (int t = 0; t < cnt; t += E * U) {
-      T va[U][V];
-      T vb[U][V];
-      int32_t ee[U];
-      bool ok[U];
+      for (int t = 0; t < cnt; t += E * U) {
+        T va[U][V];
+        T vb[U][V];
+        int32_t ee[U];
+        bool ok[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = t + slot + E * u;
-        ok[u] = j < cnt;
-        const int sl = j & 31;
-        const bool use = ok[u] && valid;
-        ee[u] = (RHO != RHO_SUM) ? __shfl_sync(kFull, eb0, sl) : 0;
-        // lhs
-        if (lm == M_FULL) {
-          gather_full<T, V>(lcol, lld, __shfl_sync(kFull, ra_lane, sl), use, va[u]);
-        } else {
-          const T sa = (lm == M_SCALAR) ? __shfl_sync(kFull, sa0, sl) : T(0);
+        for (int u = 0; u < U; ++u) {
+          const int j = t + slot + E * u;
+          ok[u] = FULLB ? true : (j < cnt);
+          const int sl = FULLB ? j : (j & 31);
+          const bool use = FULLB ? true : (ok[u] && valid);
+          ee[u] = (RHO != RHO_SUM) ? __shfl_sync(kFull, eb0, sl) : 0;
+          // lhs
+          if (lm == M_FULL) {
+            gather_full<T, V>(lcol, lld, __shfl_sync(kFull, ra_lane, sl), use, va[u]);
+          } else {
+            const T sa = (lm == M_SCALAR) ? __shfl_sync(kFull, sa0, sl) : T(0);
 #pragma unroll
-          for (int k = 0; k < V; ++k) va[u][k] = (lm == M_SCALAR) ? sa : ha[k];
+            for (int k = 0; k < V; ++k) va[u][k] = (lm == M_SCALAR) ? sa : ha[k];
+          }
+          // rhs
+          if (rm == M_FULL) {
+            gather_full<T, V>(rcol, rld, __shfl_sync(kFull, rb_lane, sl), use, vb[u]);
+          } else if (rm == M_NONE) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) vb[u][k] = T(0);
+          } else {
+            const T sb = (rm == M_SCALAR) ? __shfl_sync(kFull, sb0, sl) : T(0);
+#pragma unroll
+            for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
+          }
         }
-        // rhs
-        if (rm == M_FULL) {
-          gather_full<T, V>(rcol, rld, __shfl_sync(kFull, rb_lane, sl), use, vb[u]);
-        } else if (rm == M_NONE) {
 #pragma unroll
-          for (int k = 0; k < V; ++k) vb[u][k] = T(0);
-        } else {
-          const T sb = (rm == M_SCALAR) ? __shfl_sync(kFull, sb0, sl) : T(0);
+        for (int u = 0; u < U; ++u) {
+          if constexpr (OP == OP_DIV) {
+            bool zero = false;
 #pragma unroll
-          for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
+            for (int k = 0; k < V; ++k) zero |= valid && (vb[u][k] == T(0));
+            if (ok[u] && zero) atomicMin(a.err_pos, (int32_t)(base + t + slot + E * u));
+          }
+          if constexpr (!FULLB) {
+            // masked lanes contribute exactly nothing: a = 0 and b = 0 (1 for div)
+            const bool use = ok[u] && valid;
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              va[u][k] = use ? va[u][k] : T(0);
+              vb[u][k] = use ? vb[u][k] : (OP == OP_DIV ? T(1) : T(0));
+            }
+          }
+          acc.add(va[u], vb[u], ok[u], ee[u]);
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool use = ok[u] && valid;
-        if constexpr (OP == OP_DIV) {
-          bool zero = false;
-#pragma unroll
-          for (int k = 0; k < V; ++k) zero |= valid && (vb[u][k] == T(0));
-          if (ok[u] && zero) atomicMin(a.err_pos, (int32_t)(base + t + slot + E * u));
-        }
-        // masked lanes contribute exactly nothing: a = 0 and b = 0 (1 for div)
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          va[u][k] = use ? va[u][k] : T(0);
-          vb[u][k] = use ? vb[u][k] : (OP == OP_DIV ? T(1) : T(0));
-        }
-        acc.add(va[u], vb[u], ok[u], ee[u]);
-      }
-    }
+    };
+    if (cnt == 32 && E * U <= 32) pass(std::true_type{});
+    else pass(std::false_type{});
     if (++since_fold >= E) {  // each slot has seen <= 32 edges since the last fold
       acc.fold();
       since_fold = 0;

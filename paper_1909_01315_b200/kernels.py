@@ -405,6 +405,15 @@ def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None):
     adj = g.to_csc()
     err = _err_slot(dev) if phi.op == "div" else None
     lhs, rhs = _phi_operands(phi, X, Y, W)
+    if W is not None and phi.op != "dot" and _permute_edge_scalar(W, d_out):
+        # a per-edge scalar re-read by >= 3 column tiles: lay it out in CSC
+        # order once so every tile streams it (gmp_gather_rows)
+        Wc = _gather_rows(adj.edge_ids, W)
+        op_w = _lib.GmpOperand(_data_ptr(Wc), 1, 1, _lib.TARGETS["edge_pos"])
+        if phi.lhs_target == "edge":
+            lhs = op_w
+        else:
+            rhs = op_w
     sched = adj.schedule() if n > 0 else None
     st = lib.gmp_gspmm(ctypes.byref(_adj_struct(adj)),
                        ctypes.byref(sched.struct) if sched is not None else None,
@@ -424,6 +433,25 @@ def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None):
     if arg is not None:
         return Z, ArgExtrema(arg)
     return Z, None
+
+
+def _permute_edge_scalar(W, d_out):
+    if W.shape[1] != 1 or d_out <= 1 or W.shape[0] == 0:
+        return False
+    v = 4 if d_out % 4 == 0 else (2 if d_out % 2 == 0 else 1)
+    if W.dtype == torch.float64:
+        v = min(v, 2)
+    return -(-d_out // (32 * v)) >= 3
+
+
+def _gather_rows(idx, M):
+    """out[i] = M[idx[i]] on the device (gmp_gather_rows)."""
+    out = torch.empty((idx.numel(), M.shape[1]), dtype=M.dtype, device=M.device)
+    if out.numel():
+        _lib.check(_lib.load().gmp_gather_rows(
+            idx.numel(), M.shape[1], _dtype_code(M), idx.data_ptr(), M.data_ptr(), _ld(M),
+            out.data_ptr(), M.shape[1], _stream(M.device)), "gmp_gather_rows")
+    return out
 
 
 # ----------------------------------------------------------------------------
@@ -503,8 +531,24 @@ def extrema_backward_copy(g, aux, dZ, target, rows):
 # fused edge_softmax (replaces the 4-dispatch composition of messaging.py:105-126)
 
 
+def _softmax_call(g, fn_name, S, G2, H, out, what):
+    lib = _lib.load()
+    adj = g.to_csc()
+    sched = adj.schedule()
+    ws_bytes = int(lib.gmp_edge_softmax_workspace_size(g.num_nodes, H))
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=g.device)
+    coo = _lib.GmpCoo(g.num_nodes, g.num_edges, g.src.data_ptr(), g.dst.data_ptr())
+    args = [ctypes.byref(_adj_struct(adj)), ctypes.byref(coo), ctypes.byref(sched.struct),
+            _dtype_code(S), S.data_ptr(), _ld(S)]
+    if G2 is not None:
+        args += [G2.data_ptr(), _ld(G2)]
+    args += [H, out.data_ptr(), H, ws.data_ptr(), ws_bytes, _stream(g.device)]
+    _lib.check(getattr(lib, fn_name)(*args), what)
+
+
 def edge_softmax_forward(g, scores):
-    """alpha = per-destination softmax of (m, H) scores, one fused row kernel."""
+    """alpha = per-destination softmax of (m, H) scores: a fused per-row
+    statistics kernel plus an edge-order normalisation kernel."""
     _require_cuda(g)
     S = _as_matrix("scores", scores, g.num_edges, g.device)
     H = S.shape[1]
@@ -512,17 +556,12 @@ def edge_softmax_forward(g, scores):
                             g.num_edges, H)
     alpha = accounting.register(torch.empty((g.num_edges, H), dtype=S.dtype, device=g.device))
     if alpha.numel():
-        adj = g.to_csc()
-        sched = adj.schedule()
-        _lib.check(_lib.load().gmp_edge_softmax_fwd(
-            ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), _dtype_code(S),
-            S.data_ptr(), _ld(S), H, alpha.data_ptr(), H, _stream(g.device)),
-            "gmp_edge_softmax_fwd")
+        _softmax_call(g, "gmp_edge_softmax_fwd", S, None, H, alpha, "gmp_edge_softmax_fwd")
     return alpha
 
 
 def edge_softmax_backward(g, alpha, grad):
-    """ds = alpha * (grad - sum_{in-edges} alpha * grad), one fused row kernel."""
+    """ds = alpha * (grad - sum_{in-edges} alpha * grad), fused."""
     _require_cuda(g)
     A = _as_matrix("alpha", alpha, g.num_edges, g.device)
     Gr = _as_matrix("grad", grad, g.num_edges, g.device).to(A.dtype)
@@ -531,10 +570,5 @@ def edge_softmax_backward(g, alpha, grad):
                             g.num_edges, H)
     ds = accounting.register(torch.empty((g.num_edges, H), dtype=A.dtype, device=g.device))
     if ds.numel():
-        adj = g.to_csc()
-        sched = adj.schedule()
-        _lib.check(_lib.load().gmp_edge_softmax_bwd(
-            ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), _dtype_code(A),
-            A.data_ptr(), _ld(A), Gr.data_ptr(), _ld(Gr), H, ds.data_ptr(), H,
-            _stream(g.device)), "gmp_edge_softmax_bwd")
+        _softmax_call(g, "gmp_edge_softmax_bwd", A, Gr, H, ds, "gmp_edge_softmax_bwd")
     return ds

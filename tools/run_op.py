@@ -28,8 +28,17 @@ def main():
     p.add_argument("--time", action="store_true")
     p.add_argument("--tile-cols", type=int, default=0)
     p.add_argument("--l2mb", type=int, default=0)
+    p.add_argument("--l2fetch", type=int, default=0, help="cudaLimitMaxL2FetchGranularity bytes")
     a = p.parse_args()
     dev = torch.device("cuda")
+    torch.zeros(1, device=dev)
+    if a.l2fetch:
+        import ctypes
+        rt = ctypes.CDLL("libcudart.so.12")
+        v = ctypes.c_size_t(0)
+        rc = rt.cudaDeviceSetLimit(5, ctypes.c_size_t(a.l2fetch))
+        rt.cudaDeviceGetLimit(ctypes.byref(v), 5)
+        print("l2 fetch granularity set rc=%d now %d" % (rc, v.value))
     s, d = G.generators.power_law_edges(a.nodes, a.deg, seed=0)
     n, m, F = a.nodes, s.size, a.feat
     g = G.from_arrays(s, d, num_nodes=n, device=dev)
