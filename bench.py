@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--feat", type=int, default=FEAT)
     p.add_argument("--no-extras", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-edges", type=int, default=12_000_000,
+    p.add_argument("--cpu-edges", type=int, default=24_000_000,
                    help="edges in the CPU baseline sample (strided rows)")
     p.add_argument("--tile-cols", type=int, default=0)
     return p.parse_args()
@@ -82,7 +82,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap,utilization.gpu",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
