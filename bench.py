@@ -249,14 +249,13 @@ def main():
         tune.__enter__()
 
     if world > 1:
-        bounds = distributed.partition_rows(adj.indptr, world)
-        block = distributed.RowBlock(adj, bounds[rank], bounds[rank + 1], n)
-        x_local = X[bounds[rank]:bounds[rank + 1]].contiguous()
-        block.to_csc().schedule()
+        pg = distributed.PartitionedGraph(adj, n, rank, world)
+        x_local = X[pg.r0:pg.r1].contiguous()
+        for blk in (pg.block, pg.local_block, pg.remote_block):
+            blk.to_csc().schedule()
 
         def step():
-            xf = distributed.all_gather_rows(x_local, bounds)
-            return distributed.local_aggregate(block, xf, "sum")
+            return pg.aggregate(x_local, "sum", overlap=True)
         step_bytes = spmm_bytes(n, m, F)
     else:
         def step():
