@@ -223,11 +223,17 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # GMP_BENCH_BACKEND=gloo lets the N>1 path be smoke-tested with several
+        # ranks on one GPU; the measured configuration is NCCL, one rank per GPU
+        backend = os.environ.get("GMP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     torch.backends.cuda.matmul.allow_tf32 = False
 
     s, d, gen_s = build_graph_arrays(args)

@@ -15,8 +15,8 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 INCLUDE = HERE.parent / "include"
-BUILD = HERE.parent / "build" / "gmp"
-LIB = HERE / "libgmp.so"
+BUILD = HERE.parent / "build" / os.environ.get("GMP_BUILD_TAG", "gmp")
+LIB = Path(os.environ["GMP_LIB_OUT"]) if os.environ.get("GMP_LIB_OUT") else HERE / "libgmp.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",
@@ -50,7 +50,8 @@ def build(verbose=False, jobs=None):
 
     def compile_one(item):
         src, obj = item
-        cmd = [nvcc()] + ARCH + NVCC_FLAGS + ["-c", str(src), "-o", str(obj)]
+        extra = os.environ.get("GMP_EXTRA_FLAGS", "").split()
+        cmd = [nvcc()] + ARCH + NVCC_FLAGS + extra + ["-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -42,6 +42,9 @@
 namespace gmp {
 
 constexpr int kWarpsPerCta = 8;
+#ifndef GMP_ROW_MIN_BLOCKS
+#define GMP_ROW_MIN_BLOCKS 3
+#endif
 
 // operand access modes inside the row kernel
 enum { M_FULL = 0, M_SCALAR = 1, M_HOIST = 2, M_NONE = 3 };
@@ -435,7 +438,7 @@ struct Unroll {
 };
 
 template <typename T, int OP, int RHO, int V, int MP>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, GMP_ROW_MIN_BLOCKS)
 spmm_rows_kernel(const SpmmArgs a) {
   using Acc = RowAcc<T, OP, RHO, V>;
   using ExtT = typename Acc::ExtT;
