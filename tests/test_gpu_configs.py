@@ -1,0 +1,59 @@
+"""BASELINE.json configs C1 (Cora-shaped 2-layer GCN, 20 epochs) and C2
+(Pubmed-shaped 8-head GAT layer, forward + backward) against the
+reference's outputs (tests/golden/configs.npz, make_golden_configs.py)."""
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1909_01315_b200 as G
+from paper_1909_01315_b200 import layers
+from conftest import rel_err, to_np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+from config_inputs import SAMPLE_ROWS, c1_inputs, c2_inputs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+GOLD = Path(__file__).resolve().parent / "golden" / "configs.npz"
+
+
+@pytest.fixture(scope="module")
+def gold():
+    d = np.load(GOLD)
+    return {k: d[k] for k in d.files}
+
+
+@pytest.mark.parametrize("dtype,rtol", [(torch.float64, 1e-9), (torch.float32, 1e-5)])
+def test_c1_cora_gcn_loss_curve(gold, dtype, rtol):
+    src, dst, n, x, labels = c1_inputs()
+    g = G.from_arrays(src, dst, num_nodes=n, device=DEV)
+    model = layers.GCNModel([1433, 16, 7], seed=0, dtype=dtype)
+    xt = torch.as_tensor(x, device=DEV).to(dtype)
+    losses = layers.train(g, xt, labels, model, layers.TrainConfig(lr=0.05, epochs=20))
+    assert np.allclose(losses, gold["c1/losses"], rtol=rtol, atol=1e-7), (losses, gold["c1/losses"])
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_c2_pubmed_gat_layer_fwd_bwd(gold, dtype):
+    src, dst, n, x, u = c2_inputs()
+    g = G.from_arrays(src, dst, num_nodes=n, device=DEV)
+    params = layers.init_gat(np.random.default_rng(7), 500, 8, 8)
+    leaves = []
+    for hp in params.heads:
+        hp.W, hp.a_l, hp.a_r = (torch.as_tensor(a, device=DEV).to(dtype).requires_grad_(True)
+                                for a in (hp.W, hp.a_l, hp.a_r))
+        leaves.append((hp.W, hp.a_l, hp.a_r))
+    xt = torch.as_tensor(x, device=DEV).to(dtype)
+    h = layers.gat_layer(g, xt, params)
+    (h * torch.as_tensor(u, device=DEV).to(dtype)).sum().backward()
+    tol = 1e-10 if dtype == torch.float64 else 2e-5
+    assert rel_err(to_np(h)[SAMPLE_ROWS], gold["c2/h_rows"]) < tol
+    assert rel_err(to_np(h).sum(axis=0), gold["c2/h_colsum"]) < tol * 10
+    for i, (W, al, ar) in enumerate(leaves):
+        assert rel_err(to_np(W.grad), gold["c2/dW%d" % i]) < tol * 10, i
+        assert rel_err(to_np(al.grad), gold["c2/dal%d" % i]) < tol * 10, i
+        assert rel_err(to_np(ar.grad), gold["c2/dar%d" % i]) < tol * 10, i
