@@ -28,6 +28,7 @@ def main():
     p.add_argument("--time", action="store_true")
     p.add_argument("--tile-cols", type=int, default=0)
     p.add_argument("--l2mb", type=int, default=0)
+    p.add_argument("--rmat", type=int, default=0, help="RMAT edge count (nodes = --nodes)")
     p.add_argument("--l2fetch", type=int, default=0, help="cudaLimitMaxL2FetchGranularity bytes")
     a = p.parse_args()
     dev = torch.device("cuda")
@@ -39,14 +40,27 @@ def main():
         rc = rt.cudaDeviceSetLimit(5, ctypes.c_size_t(a.l2fetch))
         rt.cudaDeviceGetLimit(ctypes.byref(v), 5)
         print("l2 fetch granularity set rc=%d now %d" % (rc, v.value))
-    s, d = G.generators.power_law_edges(a.nodes, a.deg, seed=0)
-    n, m, F = a.nodes, s.size, a.feat
-    g = G.from_arrays(s, d, num_nodes=n, device=dev)
+    import time
+    t0 = time.time()
+    if a.rmat:
+        n = a.nodes
+        g = G.rmat(n, a.rmat, seed=0, device=dev)
+        m, F = g.num_edges, a.feat
+    else:
+        s, d = G.generators.power_law_edges(a.nodes, a.deg, seed=0)
+        n, m, F = a.nodes, s.size, a.feat
+        g = G.from_arrays(s, d, num_nodes=n, device=dev)
+    torch.cuda.synchronize()
+    t1 = time.time()
     g.to_csc().schedule()
+    torch.cuda.synchronize()
+    if a.time:
+        print("graph: n=%d m=%d gen %.1fs csc+schedule %.1fs heavy=%d" % (
+            n, m, t1 - t0, time.time() - t1, g.to_csc().schedule().n_heavy))
     gen = torch.Generator(device=dev)
     gen.manual_seed(0)
     X = torch.randn((n, F), generator=gen, device=dev)
-    W1 = torch.randn((m, 1), generator=gen, device=dev)
+    W1 = torch.randn((m, 1), generator=gen, device=dev) if a.op.startswith("umul") else None
     ops = {
         "copy_sum": lambda: G.gspmm(g, kernels.copy("src"), "sum", X=X),
         "copy_max": lambda: G.gspmm(g, kernels.copy("src"), "max", X=X),
