@@ -59,13 +59,17 @@ typedef struct {
 
 /* Degree-binned row schedule for an adjacency (built by gmp_build_schedule).
  * order: row ids sorted by degree, descending (stable). Rows order[0..n_heavy)
- * have degree > heavy_threshold and are reduced by a whole CTA; the rest by
- * one warp each. order == NULL means identity order and no CTA rows. */
+ * have degree > heavy_threshold and are reduced by a whole CTA; rows
+ * order[n_heavy..n_medium) (degree > light_threshold) by one warp each; the
+ * rest (short rows, then empty rows) several per warp, one per lane group.
+ * order == NULL means identity order, every row on the warp path. */
 typedef struct {
   const int32_t* order;
   int64_t n_heavy;
+  int64_t n_medium;
   int64_t n_nonempty;
   int32_t heavy_threshold;
+  int32_t light_threshold;
 } gmp_sched;
 
 /* COO edge list in edge-id order (graph.py:98-100). */
@@ -104,7 +108,7 @@ size_t gmp_schedule_workspace_size(int64_t n_rows);
  * (synchronises `stream` to read them back). Replaces nothing in the
  * reference (its _GroupedWalk.run walks rows in id order, kernels.py:361-373);
  * this is the degree-binned scheduling of the north star. */
-int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold,
+int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold, int32_t light_threshold,
                        int32_t* order_out, void* workspace, size_t workspace_bytes,
                        gmp_sched* sched_out, void* stream);
 

@@ -26,9 +26,9 @@ cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const
 size_t schedule_workspace_bytes(int64_t n);
 cudaError_t launch_gather_rows(int, int64_t, int32_t, const int32_t*, const void*, int64_t, void*,
                                int64_t, cudaStream_t);
-cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t* order_out,
-                           void* ws, size_t ws_bytes, int64_t* n_heavy, int64_t* n_nonempty,
-                           cudaStream_t s);
+cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t light,
+                           int32_t* order_out, void* ws, size_t ws_bytes, int64_t* n_heavy,
+                           int64_t* n_medium, int64_t* n_nonempty, cudaStream_t s);
 }  // namespace gmp
 
 using namespace gmp;
@@ -59,6 +59,13 @@ const char* op_name(int op) {
 }
 
 bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
+
+// mirrors narrow_launch<V> in spmm_rows.cuh
+bool narrow_launch_host(int V, int g_log2) {
+  const int E = 32 >> g_log2;
+  const int U = V == 4 ? 4 : 8;  // Unroll<V>
+  return E > 1 && E * U > 32;
+}
 
 int next_pow2(int x) {
   int p = 1;
@@ -213,24 +220,29 @@ int gmp_version(void) { return 1; }
 
 size_t gmp_schedule_workspace_size(int64_t n_rows) { return schedule_workspace_bytes(n_rows); }
 
-int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold, int32_t* order_out,
-                       void* workspace, size_t workspace_bytes, gmp_sched* sched_out,
-                       void* stream) {
+int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold, int32_t light_threshold,
+                       int32_t* order_out, void* workspace, size_t workspace_bytes,
+                       gmp_sched* sched_out, void* stream) {
   if (!adj || !sched_out) return fail(GMP_EINVAL, "null adjacency or schedule");
   if (adj->n_rows < 0 || adj->n_rows >= (1ll << 31)) return fail(GMP_EINVAL, "n_rows out of range");
   if (adj->n_rows > 0 && (!order_out || !adj->indptr)) return fail(GMP_EINVAL, "null arrays");
   if (workspace_bytes < schedule_workspace_bytes(adj->n_rows))
     return fail(GMP_EINVAL, "workspace too small: %zu < %zu", workspace_bytes,
                 schedule_workspace_bytes(adj->n_rows));
-  int64_t nh = 0, nn = 0;
-  cudaError_t e = build_schedule(adj->n_rows, adj->indptr, heavy_threshold, order_out, workspace,
-                                 workspace_bytes, &nh, &nn, (cudaStream_t)stream);
+  if (light_threshold < 0 || light_threshold > heavy_threshold)
+    return fail(GMP_EINVAL, "light threshold must be in [0, heavy threshold]");
+  int64_t nh = 0, nm = 0, nn = 0;
+  cudaError_t e = build_schedule(adj->n_rows, adj->indptr, heavy_threshold, light_threshold,
+                                 order_out, workspace, workspace_bytes, &nh, &nm, &nn,
+                                 (cudaStream_t)stream);
   g_launches += adj->n_rows > 0 ? 2 : 0;
   if (e != cudaSuccess) return cuda_status(e, "gmp_build_schedule");
   sched_out->order = order_out;
   sched_out->n_heavy = nh;
+  sched_out->n_medium = nm;
   sched_out->n_nonempty = nn;
   sched_out->heavy_threshold = heavy_threshold;
+  sched_out->light_threshold = light_threshold;
   return GMP_OK;
 }
 
@@ -297,9 +309,19 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
   const int G = std::min(32, next_pow2((tw + V - 1) / V));
   const int ntiles = (d_out + tw - 1) / tw;
 
+  // short rows share a warp (one per lane group) when a row uses fewer than
+  // 32 lanes; otherwise every non-heavy row gets a warp
+  const int E = 32 / G;
+  const bool narrow = (F == 4) && narrow_launch_host(V, log2i(G));
+  const int64_t n_medium = (order && narrow) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
+  const int64_t medium_blocks = (n_medium - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int64_t light_rows = adj->n_rows - n_medium;
+  const int64_t bpt_rows = n_heavy + medium_blocks +
+                           (light_rows + (int64_t)kWarpsPerCta * E - 1) / ((int64_t)kWarpsPerCta * E);
   SpmmArgs a{};
   a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
-  a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.blocks_per_tile = bpt;
+  a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_medium;
+  a.medium_blocks = medium_blocks; a.blocks_per_tile = bpt_rows;
   a.d_out = d_out; a.tile_cols = tw; a.g_log2 = log2i(G); a.mean = rho == GMP_MEAN;
   a.lhs = row_operand(ops[0]);
   a.rhs = row_operand(ops[1]);
@@ -318,7 +340,7 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
   a.need_eid = ext || (a.lhs.from_eid && a.lhs.mode != M_HOIST) ||
                (ops[1].present && a.rhs.from_eid && a.rhs.mode != M_HOIST);
   a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts; a.err_pos = err_pos;
-  const int64_t grid = bpt * ntiles;
+  const int64_t grid = bpt_rows * ntiles;
   if (grid >= (1ll << 31)) return fail(GMP_EUNSUPPORTED, "grid too large");
   switch (kop) {
     case OP_COPY: e = launch_spmm_rows<OP_COPY>(F == 8, krho, V, mp, a, grid, s); break;

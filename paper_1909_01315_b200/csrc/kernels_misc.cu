@@ -184,8 +184,9 @@ cudaError_t launch_gather_rows(int f64, int64_t n, int32_t dim, const int32_t* i
 // ---- degree-binned schedule ---------------------------------------------------
 
 __global__ void degree_kernel(int64_t n, const int64_t* __restrict__ indptr, int32_t* deg,
-                              int32_t* rows, int32_t thr, unsigned long long* counters) {
-  unsigned long long heavy = 0, nonempty = 0;
+                              int32_t* rows, int32_t thr, int32_t light,
+                              unsigned long long* counters) {
+  unsigned long long heavy = 0, nonempty = 0, medium = 0;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t dg = indptr[r + 1] - indptr[r];
@@ -193,14 +194,17 @@ __global__ void degree_kernel(int64_t n, const int64_t* __restrict__ indptr, int
     rows[r] = (int32_t)r;
     heavy += dg > thr;
     nonempty += dg > 0;
+    medium += dg > light;
   }
   for (int off = 16; off > 0; off >>= 1) {
     heavy += __shfl_xor_sync(kFull, heavy, off);
     nonempty += __shfl_xor_sync(kFull, nonempty, off);
+    medium += __shfl_xor_sync(kFull, medium, off);
   }
   if ((threadIdx.x & 31) == 0) {
     if (heavy) atomicAdd(counters, heavy);
     if (nonempty) atomicAdd(counters + 1, nonempty);
+    if (medium) atomicAdd(counters + 2, medium);
   }
 }
 
@@ -215,15 +219,15 @@ size_t schedule_cub_bytes(int64_t n) {
 }
 
 size_t schedule_workspace_bytes(int64_t n) {
-  return align256(16) + 3 * align256((size_t)n * 4) + align256(schedule_cub_bytes(n));
+  return align256(32) + 3 * align256((size_t)n * 4) + align256(schedule_cub_bytes(n));
 }
 
-cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t* order_out,
-                           void* ws, size_t ws_bytes, int64_t* n_heavy, int64_t* n_nonempty,
-                           cudaStream_t s) {
+cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t light,
+                           int32_t* order_out, void* ws, size_t ws_bytes, int64_t* n_heavy,
+                           int64_t* n_medium, int64_t* n_nonempty, cudaStream_t s) {
   char* p = static_cast<char*>(ws);
   auto* counters = reinterpret_cast<unsigned long long*>(p);
-  p += align256(16);
+  p += align256(32);
   auto* deg = reinterpret_cast<int32_t*>(p);
   p += align256((size_t)n * 4);
   auto* deg_sorted = reinterpret_cast<int32_t*>(p);
@@ -231,21 +235,22 @@ cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_
   auto* rows = reinterpret_cast<int32_t*>(p);
   p += align256((size_t)n * 4);
   size_t cub_bytes = ws_bytes - (size_t)(p - static_cast<char*>(ws));
-  cudaError_t err = cudaMemsetAsync(counters, 0, 16, s);
+  cudaError_t err = cudaMemsetAsync(counters, 0, 32, s);
   if (err != cudaSuccess) return err;
   if (n > 0) {
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    degree_kernel<<<grid, 256, 0, s>>>(n, indptr, deg, rows, thr, counters);
+    degree_kernel<<<grid, 256, 0, s>>>(n, indptr, deg, rows, thr, light, counters);
     err = cub::DeviceRadixSort::SortPairsDescending(p, cub_bytes, deg, deg_sorted, rows, order_out,
                                                     (int)n, 0, 32, s);
     if (err != cudaSuccess) return err;
   }
-  unsigned long long host[2] = {0, 0};
-  err = cudaMemcpyAsync(host, counters, 16, cudaMemcpyDeviceToHost, s);
+  unsigned long long host[3] = {0, 0, 0};
+  err = cudaMemcpyAsync(host, counters, 24, cudaMemcpyDeviceToHost, s);
   if (err != cudaSuccess) return err;
   err = cudaStreamSynchronize(s);
   *n_heavy = (int64_t)host[0];
   *n_nonempty = (int64_t)host[1];
+  *n_medium = (int64_t)host[2];
   return err;
 }
 

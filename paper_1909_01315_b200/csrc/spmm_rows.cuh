@@ -67,6 +67,8 @@ struct SpmmArgs {
   const int32_t* order;  // nullable: identity order
   int64_t n_rows;
   int64_t n_heavy;
+  int64_t n_medium;       // rows [n_heavy, n_medium) of `order`: one warp each
+  int64_t medium_blocks;  // CTAs covering them (kWarpsPerCta rows per CTA)
   int64_t blocks_per_tile;
   int32_t d_out;
   int32_t tile_cols;
@@ -406,6 +408,188 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
   acc.fold();
 }
 
+// Narrow rows (E * U > 32 edge slots per warp step, i.e. d < 16): a 32-edge
+// batch gives each lane fewer than U gathers, so edge ids are staged in
+// shared memory kChunkE at a time (coalesced, one chunk ahead) and every
+// lane keeps U independent gathers in flight.
+constexpr int kChunkE = 256;
+
+template <typename T, int OP, int RHO, int V, int MP, int U>
+__device__ __forceinline__ void spmm_accumulate_chunked(
+    const SpmmArgs& a, int64_t pb, int64_t pe, int64_t first, int64_t stride, int lane, int slot,
+    int E, int col, bool valid, const T (&ha)[V], const T (&hb)[V], int32_t* sidx,
+    int32_t* seid, RowAcc<T, OP, RHO, V>& acc) {
+  constexpr bool BIN = OP != OP_COPY;
+  constexpr int B = kChunkE / 32;
+  const int lm = (MP == MP_GEN) ? a.lhs.mode : M_FULL;
+  const int rm = !BIN ? M_NONE
+                      : (MP == MP_FF ? M_FULL
+                                     : (MP == MP_FS ? M_SCALAR
+                                                    : (MP == MP_FH ? M_HOIST : a.rhs.mode)));
+  const bool need_eid = a.need_eid;
+  const int ccol = valid ? col : 0;
+  const T* lcol = static_cast<const T*>(a.lhs.data) + ccol;
+  const T* rcol = BIN ? static_cast<const T*>(a.rhs.data) + ccol : nullptr;
+  const uint32_t lld = a.lhs.ld * (uint32_t)sizeof(T);
+  const uint32_t rld = a.rhs.ld * (uint32_t)sizeof(T);
+  int32_t pn[B], pe_[B];
+  auto fetch = [&](int64_t cb) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const int64_t q = cb + i * 32 + lane;
+      pn[i] = q < pe ? __ldg(a.indices + q) : 0;
+      pe_[i] = (q < pe && need_eid) ? __ldg(a.eids + q) : 0;
+    }
+  };
+  fetch(pb + first);
+  int since_fold = 0;
+  for (int64_t cb = pb + first; cb < pe; cb += stride) {
+    const int cnt = (int)min((int64_t)kChunkE, pe - cb);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      sidx[i * 32 + lane] = pn[i];
+      seid[i * 32 + lane] = pe_[i];
+    }
+    __syncwarp();
+    fetch(cb + stride);
+#pragma unroll 1
+    for (int t = 0; t < cnt; t += E * U) {
+      T va[U][V], vb[U][V];
+      int32_t ee[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = t + slot + E * u;
+        ok[u] = j < cnt;
+        const int jj = ok[u] ? j : 0;
+        const int32_t nb = sidx[jj];
+        const int32_t eb = seid[jj];
+        ee[u] = eb;
+        const int64_t p = cb + jj;
+        const uint32_t ra = a.lhs.from_pos ? (uint32_t)p : (uint32_t)(a.lhs.from_eid ? eb : nb);
+        const uint32_t rb = a.rhs.from_pos ? (uint32_t)p : (uint32_t)(a.rhs.from_eid ? eb : nb);
+        const bool use = ok[u] && valid;
+        if (lm == M_FULL) {
+          gather_full<T, V>(lcol, lld, ra, use, va[u]);
+        } else {
+          const T sa = (lm == M_SCALAR && ok[u]) ? scalar_at<T>(a.lhs, ra) : T(0);
+#pragma unroll
+          for (int k = 0; k < V; ++k) va[u][k] = (lm == M_SCALAR) ? sa : ha[k];
+        }
+        if (rm == M_FULL) {
+          gather_full<T, V>(rcol, rld, rb, use, vb[u]);
+        } else if (rm == M_NONE) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) vb[u][k] = T(0);
+        } else {
+          const T sb = (rm == M_SCALAR && ok[u]) ? scalar_at<T>(a.rhs, rb) : T(0);
+#pragma unroll
+          for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool use = ok[u] && valid;
+        if constexpr (OP == OP_DIV) {
+          bool zero = false;
+#pragma unroll
+          for (int k = 0; k < V; ++k) zero |= valid && (vb[u][k] == T(0));
+          if (ok[u] && zero) atomicMin(a.err_pos, (int32_t)(cb + t + slot + E * u));
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          va[u][k] = use ? va[u][k] : T(0);
+          vb[u][k] = use ? vb[u][k] : (OP == OP_DIV ? T(1) : T(0));
+        }
+        acc.add(va[u], vb[u], ok[u], ee[u]);
+      }
+    }
+    since_fold += (cnt + E - 1) / E;  // edges each slot added from this chunk
+    if (since_fold + kChunkE / E > 32) {  // fold before a slot could pass 32 edges
+      acc.fold();
+      since_fold = 0;
+    }
+  }
+  acc.fold();
+}
+
+// Short rows (<= light threshold edges): each lane group (slot) of the warp
+// owns one row and walks its edges itself - E rows per warp, so a warp is not
+// tied up by a row of a handful of edges. Rows arrive degree-sorted, so the
+// slots of a warp have near-equal lengths.
+template <typename T, int OP, int RHO, int V, int MP, int U>
+__device__ __forceinline__ void spmm_accumulate_slot(const SpmmArgs& a, int64_t pb, int64_t pe,
+                                                     int col, bool valid, const T (&ha)[V],
+                                                     const T (&hb)[V],
+                                                     RowAcc<T, OP, RHO, V>& acc) {
+  constexpr bool BIN = OP != OP_COPY;
+  const int lm = (MP == MP_GEN) ? a.lhs.mode : M_FULL;
+  const int rm = !BIN ? M_NONE
+                      : (MP == MP_FF ? M_FULL
+                                     : (MP == MP_FS ? M_SCALAR
+                                                    : (MP == MP_FH ? M_HOIST : a.rhs.mode)));
+  const bool need_eid = a.need_eid;
+  const int ccol = valid ? col : 0;
+  const T* lcol = static_cast<const T*>(a.lhs.data) + ccol;
+  const T* rcol = BIN ? static_cast<const T*>(a.rhs.data) + ccol : nullptr;
+  const uint32_t lld = a.lhs.ld * (uint32_t)sizeof(T);
+  const uint32_t rld = a.rhs.ld * (uint32_t)sizeof(T);
+  const int cnt = (int)(pe - pb);
+  const int max_cnt = __reduce_max_sync(kFull, (unsigned)cnt);
+  for (int t = 0; t < max_cnt; t += U) {
+    T va[U][V], vb[U][V];
+    int32_t ee[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = t + u;
+      ok[u] = j < cnt;
+      const int64_t p = pb + (ok[u] ? j : 0);
+      const int32_t nb = ok[u] ? __ldg(a.indices + p) : 0;
+      const int32_t eb = (ok[u] && need_eid) ? __ldg(a.eids + p) : 0;
+      ee[u] = eb;
+      const uint32_t ra = a.lhs.from_pos ? (uint32_t)p : (uint32_t)(a.lhs.from_eid ? eb : nb);
+      const uint32_t rb = a.rhs.from_pos ? (uint32_t)p : (uint32_t)(a.rhs.from_eid ? eb : nb);
+      const bool use = ok[u] && valid;
+      if (lm == M_FULL) {
+        gather_full<T, V>(lcol, lld, ra, use, va[u]);
+      } else {
+        const T sa = (lm == M_SCALAR && ok[u]) ? scalar_at<T>(a.lhs, ra) : T(0);
+#pragma unroll
+        for (int k = 0; k < V; ++k) va[u][k] = (lm == M_SCALAR) ? sa : ha[k];
+      }
+      if (rm == M_FULL) {
+        gather_full<T, V>(rcol, rld, rb, use, vb[u]);
+      } else if (rm == M_NONE) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) vb[u][k] = T(0);
+      } else {
+        const T sb = (rm == M_SCALAR && ok[u]) ? scalar_at<T>(a.rhs, rb) : T(0);
+#pragma unroll
+        for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool use = ok[u] && valid;
+      if constexpr (OP == OP_DIV) {
+        bool zero = false;
+#pragma unroll
+        for (int k = 0; k < V; ++k) zero |= valid && (vb[u][k] == T(0));
+        if (ok[u] && zero) atomicMin(a.err_pos, (int32_t)(pb + t + u));
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        va[u][k] = use ? va[u][k] : T(0);
+        vb[u][k] = use ? vb[u][k] : (OP == OP_DIV ? T(1) : T(0));
+      }
+      acc.add(va[u], vb[u], ok[u], ee[u]);
+    }
+  }
+  acc.fold();
+}
+
 template <typename T, int OP, int RHO, int V>
 __device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_t deg, int col,
                                           bool valid, const RowAcc<T, OP, RHO, V>& acc) {
@@ -437,7 +621,11 @@ struct Unroll {
   static constexpr int value = V == 4 ? 4 : 8;
 };
 
-template <typename T, int OP, int RHO, int V, int MP>
+// NARROW: rows use few lanes (E > 1 and E*U > 32, i.e. d < 16): short rows
+// share a warp and longer rows stage edge ids in shared memory. Wide kernels
+// (every d >= 16 with V=4, and all fp64 launches) compile without those paths
+// so their main loop is scheduled on its own.
+template <typename T, int OP, int RHO, int V, int MP, bool NARROW>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, GMP_ROW_MIN_BLOCKS)
 spmm_rows_kernel(const SpmmArgs a) {
   using Acc = RowAcc<T, OP, RHO, V>;
@@ -447,6 +635,7 @@ spmm_rows_kernel(const SpmmArgs a) {
   __shared__ double s_acc[RHO == RHO_SUM ? kWarpsPerCta : 1][kCols];
   __shared__ ExtT s_cur[RHO == RHO_SUM ? 1 : kWarpsPerCta][kCols];
   __shared__ int32_t s_arg[RHO == RHO_SUM ? 1 : kWarpsPerCta][kCols];
+  extern __shared__ int32_t s_chunk[];  // [2][kWarpsPerCta][kChunkE], only for chunked launches
 
   const int64_t bid = blockIdx.x;
   const int tile = (int)(bid / a.blocks_per_tile);
@@ -460,17 +649,23 @@ spmm_rows_kernel(const SpmmArgs a) {
   const int slot = lane >> a.g_log2;
   const int gl = lane & (G - 1);
   const bool heavy = local < a.n_heavy;  // block-uniform
+  const bool light = NARROW && local >= a.n_heavy + a.medium_blocks;  // block-uniform
 
   int64_t row;
   if (heavy) {
     row = a.order[local];
-  } else {
+  } else if (!light) {
     const int64_t r = a.n_heavy + (local - a.n_heavy) * kWarpsPerCta + warp;
-    if (r >= a.n_rows) return;  // light mode never synchronises the CTA
+    if (r >= a.n_medium) return;  // warp rows never synchronise the CTA
     row = a.order ? (int64_t)a.order[r] : r;
+  } else {
+    const int64_t r = a.n_medium +
+                      ((local - a.n_heavy - a.medium_blocks) * kWarpsPerCta + warp) * E + slot;
+    if (__all_sync(kFull, r >= a.n_rows)) return;
+    row = r < a.n_rows ? (a.order ? (int64_t)a.order[r] : r) : -1;  // -1: idle slot
   }
-  const int64_t pb = a.indptr[row];
-  const int64_t pe = a.indptr[row + 1];
+  const int64_t pb = row >= 0 ? a.indptr[row] : 0;
+  const int64_t pe = row >= 0 ? a.indptr[row + 1] : 0;
   const int64_t deg = pe - pb;
   const int col = c0 + gl * V;
   const bool valid = col < c1;
@@ -491,7 +686,19 @@ spmm_rows_kernel(const SpmmArgs a) {
 
   Acc acc;
   acc.init();
-  if (heavy) {
+  if constexpr (NARROW) {
+    if (light) {
+      spmm_accumulate_slot<T, OP, RHO, V, MP, U>(a, pb, pe, col, valid, ha, hb, acc);
+      if (row < 0) return;
+      if (a.counts && tile == 0 && gl == 0) a.counts[row] = deg;
+      write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
+      return;
+    }
+    spmm_accumulate_chunked<T, OP, RHO, V, MP, U>(
+        a, pb, pe, heavy ? (int64_t)warp * kChunkE : 0,
+        heavy ? (int64_t)kChunkE * kWarpsPerCta : kChunkE, lane, slot, E, col, valid, ha, hb,
+        s_chunk + warp * kChunkE, s_chunk + (kWarpsPerCta + warp) * kChunkE, acc);
+  } else if (heavy) {
     spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, (int64_t)warp * 32, 32 * kWarpsPerCta, lane,
                                           slot, E, col, valid, ha, hb, acc);
   } else {
@@ -539,9 +746,21 @@ spmm_rows_kernel(const SpmmArgs a) {
   }
 }
 
+template <int V>
+__host__ __device__ constexpr bool narrow_launch(int g_log2) {
+  return (32 >> g_log2) > 1 && (32 >> g_log2) * Unroll<V>::value > 32;
+}
+
 template <typename T, int OP, int RHO, int V, int MP>
 cudaError_t launch_spmm_rows_t(const SpmmArgs& a, int64_t grid, cudaStream_t s) {
-  spmm_rows_kernel<T, OP, RHO, V, MP><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
+  if constexpr (sizeof(T) == 4) {
+    if (narrow_launch<V>(a.g_log2)) {
+      spmm_rows_kernel<T, OP, RHO, V, MP, true>
+          <<<(unsigned)grid, kWarpsPerCta * 32, 2 * kWarpsPerCta * kChunkE * sizeof(int32_t), s>>>(a);
+      return cudaGetLastError();
+    }
+  }
+  spmm_rows_kernel<T, OP, RHO, V, MP, false><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 

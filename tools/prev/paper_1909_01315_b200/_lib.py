@@ -33,8 +33,7 @@ class GmpAdj(ctypes.Structure):
 
 class GmpSched(ctypes.Structure):
     _fields_ = [("order", ctypes.c_void_p), ("n_heavy", ctypes.c_int64),
-                ("n_medium", ctypes.c_int64), ("n_nonempty", ctypes.c_int64),
-                ("heavy_threshold", ctypes.c_int32), ("light_threshold", ctypes.c_int32)]
+                ("n_nonempty", ctypes.c_int64), ("heavy_threshold", ctypes.c_int32)]
 
 
 class GmpCoo(ctypes.Structure):
@@ -66,8 +65,7 @@ def _declare(lib):
     c_int = ctypes.c_int
     lib.gmp_schedule_workspace_size.argtypes = [i64]
     lib.gmp_schedule_workspace_size.restype = ctypes.c_size_t
-    lib.gmp_build_schedule.argtypes = [_P(GmpAdj), i32, i32, vp, vp, ctypes.c_size_t,
-                                       _P(GmpSched), vp]
+    lib.gmp_build_schedule.argtypes = [_P(GmpAdj), i32, vp, vp, ctypes.c_size_t, _P(GmpSched), vp]
     lib.gmp_gspmm.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, c_int, c_int,
                               _P(GmpOperand), _P(GmpOperand), vp, i64, i32, vp, vp, vp,
                               _P(GmpTuning), vp]

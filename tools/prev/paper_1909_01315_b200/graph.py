@@ -30,10 +30,8 @@ import torch
 _uid = itertools.count(1)
 _INT32_LIMIT = 2 ** 31 - 1
 
-# rows with more in-edges than this are reduced by a whole CTA (gmp_sched);
-# rows with at most LIGHT_ROW_THRESHOLD in-edges share a warp (one per lane group)
+# rows with more in-edges than this are reduced by a whole CTA (gmp_sched)
 HEAVY_ROW_THRESHOLD = 2048
-LIGHT_ROW_THRESHOLD = 32
 
 
 def default_device():

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib, accounting
-from .graph import HEAVY_ROW_THRESHOLD, LIGHT_ROW_THRESHOLD
+from .graph import HEAVY_ROW_THRESHOLD
 
 BLOCK_EDGES = 2048  # reference chunk size (kernels.py:39); device kernels need no host chunking
 
@@ -316,7 +316,7 @@ def _adj_struct(adj):
 
 
 class _Schedule:
-    __slots__ = ("struct", "order", "n_heavy", "n_medium", "n_nonempty")
+    __slots__ = ("struct", "order", "n_heavy", "n_nonempty")
 
 
 def _build_schedule(adj):
@@ -329,12 +329,11 @@ def _build_schedule(adj):
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     sched = _lib.GmpSched()
     _lib.check(lib.gmp_build_schedule(ctypes.byref(_adj_struct(adj)), HEAVY_ROW_THRESHOLD,
-                                      LIGHT_ROW_THRESHOLD, order.data_ptr(), ws.data_ptr(), ws_bytes,
+                                      order.data_ptr(), ws.data_ptr(), ws_bytes,
                                       ctypes.byref(sched), _stream(dev)), "gmp_build_schedule")
     out = _Schedule()
     out.struct, out.order = sched, order
     out.n_heavy, out.n_nonempty = int(sched.n_heavy), int(sched.n_nonempty)
-    out.n_medium = int(sched.n_medium)
     return out
 
 

@@ -1,0 +1,245 @@
+"""GCN / GraphSAGE / GAT as thin torch callers of the g-SpMM / g-SDDMM kernels.
+
+These exist to time and check the epoch configs (BASELINE.json configs 0-3);
+they own no kernels. Semantics follow /root/reference/pkg/src/graphmp/layers.py:
+  gcn_layer  act(mean_agg(X) @ W + b)          (layers.py:62-67; aggregate first)
+  sage_layer act(X @ W_self + mean_agg(X) @ W_neigh)   (layers.py:76-81)
+  gat_layer  per head: proj = X @ W; score_uv = a_l.proj_u + a_r.proj_v (u_add_v
+             g-SDDMM, no LeakyReLU); alpha = edge_softmax; out = sum_u alpha*proj_u
+             (u_mul_e g-SpMM); heads concatenated            (layers.py:96-116)
+`aggregator="sum"` gives the copy_u+sum GCN named by BASELINE.json config 0.
+Dense projections are torch matmuls (cuBLAS; fp32 with TF32 off by default so
+parity tests compare against the reference's float64 numbers).
+The GAT head scores are computed for all heads in one u_add_v g-SDDMM and
+one fused edge_softmax over (m, H); the per-head u_mul_e aggregations read
+strided column views of the (n, H*D) projection, so no head copy is made.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import autodiff, kernels
+from .graph import default_device
+
+RELU_GAIN = float(np.sqrt(2.0))
+
+
+def xavier_uniform(rng, fan_in, fan_out, gain=RELU_GAIN):
+    """Uniform on [-a, a], a = gain * sqrt(6 / (fan_in + fan_out)) (layers.py:31-34)."""
+    a = gain * np.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-a, a, size=(fan_in, fan_out))
+
+
+def _act(h, name):
+    if name == "relu":
+        return torch.relu(h)
+    if name in (None, "linear"):
+        return h
+    raise ValueError("unknown activation %r" % (name,))
+
+
+def _check_rows(g, X):
+    if X.shape[0] != g.num_nodes:
+        raise ValueError("feature matrix has %d rows for a %d-node graph"
+                         % (X.shape[0], g.num_nodes))
+
+
+def _t(x, device, dtype):
+    if torch.is_tensor(x):
+        return x
+    return torch.as_tensor(np.asarray(x), dtype=dtype, device=device)
+
+
+def aggregate(g, X, aggregator="mean", **kw):
+    """copy_u g-SpMM with the given reducer (mean = in-degree normalised)."""
+    return autodiff.gspmm(g, kernels.copy("src"), aggregator, X=X, **kw)
+
+
+@dataclass
+class GCNParams:
+    W: torch.Tensor
+    b: torch.Tensor
+
+
+@dataclass
+class SAGEParams:
+    W_self: torch.Tensor
+    W_neigh: torch.Tensor
+
+
+@dataclass
+class GATHead:
+    W: torch.Tensor
+    a_l: torch.Tensor
+    a_r: torch.Tensor
+
+
+@dataclass
+class GATParams:
+    heads: list
+
+
+def gcn_layer(g, X, params, act="relu", aggregator="mean", **kw):
+    _check_rows(g, X)
+    agg = aggregate(g, X, aggregator, **kw)
+    W = _t(params.W, agg.device, agg.dtype)
+    b = _t(params.b, agg.device, agg.dtype)
+    return _act(agg @ W + b, act)
+
+
+def sage_layer(g, X, params, act="relu", **kw):
+    _check_rows(g, X)
+    X = _t(X, g.device, torch.float64)
+    Ws = _t(params.W_self, X.device, X.dtype)
+    Wn = _t(params.W_neigh, X.device, X.dtype)
+    return _act(X @ Ws + aggregate(g, X, "mean", **kw) @ Wn, act)
+
+
+def gat_layer(g, X, params, num_heads=None, **kw):
+    """Heads concatenated column-wise; isolated destinations get zero rows."""
+    _check_rows(g, X)
+    heads = params.heads if num_heads is None else params.heads[:num_heads]
+    if not heads:
+        raise ValueError("head count must be >= 1")
+    X = _t(X, g.device, torch.float64)
+    dev, dt = X.device, X.dtype
+    Wcat = torch.cat([_t(h.W, dev, dt) for h in heads], dim=1)           # (d_in, H*D)
+    D = _t(heads[0].W, dev, dt).shape[1]
+    H = len(heads)
+    proj = X @ Wcat                                                       # (n, H*D)
+    pv = proj.view(-1, H, D)
+    al = torch.stack([_t(h.a_l, dev, dt)[:, 0] for h in heads])           # (H, D)
+    ar = torch.stack([_t(h.a_r, dev, dt)[:, 0] for h in heads])
+    el = (pv * al).sum(-1)                                                # (n, H)
+    er = (pv * ar).sum(-1)
+    score = autodiff.gsddmm(g, kernels.add("src", "dst"), X=el, Y=er, **kw)   # (m, H)
+    alpha = autodiff.edge_softmax(g, score)
+    outs = [autodiff.gspmm(g, kernels.mul("src", "edge"), "sum",
+                           X=proj[:, h * D:(h + 1) * D], W=alpha[:, h:h + 1], **kw)
+            for h in range(H)]
+    return outs[0] if H == 1 else torch.cat(outs, dim=1)
+
+
+def init_gcn(rng, d_in, d_out):
+    return GCNParams(W=xavier_uniform(rng, d_in, d_out), b=np.zeros((1, d_out)))
+
+
+def init_sage(rng, d_in, d_out):
+    return SAGEParams(W_self=xavier_uniform(rng, d_in, d_out),
+                      W_neigh=xavier_uniform(rng, d_in, d_out))
+
+
+def init_gat(rng, d_in, d_head, num_heads):
+    return GATParams(heads=[GATHead(W=xavier_uniform(rng, d_in, d_head),
+                                    a_l=xavier_uniform(rng, d_head, 1),
+                                    a_r=xavier_uniform(rng, d_head, 1))
+                            for _ in range(num_heads)])
+
+
+def _leaf(a, device, dtype):
+    return torch.as_tensor(np.asarray(a), dtype=dtype, device=device).requires_grad_(True)
+
+
+class GCNModel:
+    """Stack of GCN layers (relu between, linear last); numpy-seeded init
+    identical to the reference's GCNModel (layers.py:137-158)."""
+
+    def __init__(self, dims, seed=0, aggregator="mean", device=None, dtype=torch.float32):
+        if len(dims) < 2:
+            raise ValueError("need at least input and output dims")
+        rng = np.random.default_rng(seed)
+        device = device or default_device()
+        self.aggregator = aggregator
+        self.layers = []
+        for a, b in zip(dims, dims[1:]):
+            p = init_gcn(rng, a, b)
+            self.layers.append(GCNParams(W=_leaf(p.W, device, dtype), b=_leaf(p.b, device, dtype)))
+
+    def parameters(self):
+        return [t for lp in self.layers for t in (lp.W, lp.b)]
+
+    def forward(self, g, x, **kw):
+        h = x
+        last = len(self.layers) - 1
+        for i, p in enumerate(self.layers):
+            h = gcn_layer(g, h, p, act="relu" if i < last else "linear",
+                          aggregator=self.aggregator, **kw)
+        return h
+
+
+class SAGEModel:
+    """Stack of GraphSAGE-mean layers."""
+
+    def __init__(self, dims, seed=0, device=None, dtype=torch.float32):
+        rng = np.random.default_rng(seed)
+        device = device or default_device()
+        self.layers = []
+        for a, b in zip(dims, dims[1:]):
+            p = init_sage(rng, a, b)
+            self.layers.append(SAGEParams(W_self=_leaf(p.W_self, device, dtype),
+                                          W_neigh=_leaf(p.W_neigh, device, dtype)))
+
+    def parameters(self):
+        return [t for lp in self.layers for t in (lp.W_self, lp.W_neigh)]
+
+    def forward(self, g, x, **kw):
+        h = x
+        last = len(self.layers) - 1
+        for i, p in enumerate(self.layers):
+            h = sage_layer(g, h, p, act="relu" if i < last else "linear", **kw)
+        return h
+
+
+@dataclass
+class TrainConfig:
+    lr: float = 0.05
+    epochs: int = 100
+    seed: int = 0
+    strategy: str = None
+
+    def __post_init__(self):
+        if self.lr < 0:
+            raise ValueError("learning rate must be non-negative")
+        if self.epochs < 1:
+            raise ValueError("epochs must be >= 1")
+
+
+def xent_loss(logits, labels):
+    """Mean cross-entropy of row-softmax probabilities (autodiff.py:228-246)."""
+    return F.cross_entropy(logits, labels)
+
+
+def train_epoch(g, x, labels, model, lr):
+    """One full-graph gradient-descent step; returns the loss tensor (on device)."""
+    params = model.parameters()
+    loss = xent_loss(model.forward(g, x), labels)
+    grads = torch.autograd.grad(loss, params)
+    with torch.no_grad():
+        for p, gr in zip(params, grads):
+            p.sub_(lr * gr)
+    return loss.detach()
+
+
+def train(g, features, labels, model, cfg):
+    """Full-graph gradient descent; per-epoch losses (layers.py:175-202)."""
+    params = model.parameters()
+    dev, dt = params[0].device, params[0].dtype
+    x = features if torch.is_tensor(features) else torch.as_tensor(
+        np.asarray(features), dtype=dt, device=dev)
+    labels = torch.as_tensor(np.asarray(labels.cpu() if torch.is_tensor(labels) else labels),
+                             dtype=torch.int64, device=dev)
+    n_classes = params[-1].shape[1]
+    if int(labels.min()) < 0 or int(labels.max()) >= n_classes:
+        raise ValueError("label out of range [0, %d)" % n_classes)
+    losses = []
+    for _ in range(cfg.epochs):
+        if cfg.strategy is not None:
+            with kernels.force_strategy(cfg.strategy):
+                loss = train_epoch(g, x, labels, model, cfg.lr)
+        else:
+            loss = train_epoch(g, x, labels, model, cfg.lr)
+        losses.append(loss)
+    return [float(v) for v in torch.stack(losses).cpu()]
