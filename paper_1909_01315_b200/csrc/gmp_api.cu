@@ -63,7 +63,7 @@ bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(
 // mirrors narrow_launch<V> in spmm_rows.cuh
 bool narrow_launch_host(int V, int g_log2) {
   const int E = 32 >> g_log2;
-  const int U = V == 4 ? 4 : 8;  // Unroll<V>
+  const int U = Unroll<4>::value;  // Unroll<V> is 8 for every V
   return E > 1 && E * U > 32;
 }
 
