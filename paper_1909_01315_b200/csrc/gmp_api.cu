@@ -288,6 +288,36 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
     if (L->target == GMP_EDGE_POS || (R && R->target == GMP_EDGE_POS))
       return fail(GMP_EINVAL, "dot messages take edge operands in edge-id order");
     const int dim = L->dim;
+    const int Vd = dim > 0 ? pick_v(F, dim, ops, 2, nullptr, 0, nullptr) : 1;
+    if (!ext && dim > 0 && dim <= 32 * Vd) {
+      // sum / mean of dots == sum of per-column products: the row kernel
+      // accumulates them per column and reduces the columns at the end
+      const int Gd = std::min(32, next_pow2((dim + Vd - 1) / Vd));
+      const bool narrow = (F == 4) && narrow_launch_host(Vd, log2i(Gd));
+      const int64_t n_med = (order && narrow) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
+      const int64_t med_blocks = (n_med - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
+      const int64_t rows_per_light_cta = (int64_t)kWarpsPerCta * (32 / Gd);
+      SpmmArgs a{};
+      a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
+      a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_med;
+      a.medium_blocks = med_blocks;
+      a.blocks_per_tile = n_heavy + med_blocks +
+                          (adj->n_rows - n_med + rows_per_light_cta - 1) / rows_per_light_cta;
+      a.d_out = dim; a.tile_cols = dim; a.g_log2 = log2i(Gd); a.mean = rho == GMP_MEAN;
+      a.lhs = row_operand(ops[0]);
+      a.rhs = row_operand(ops[1]);
+      a.lhs.bcast = a.rhs.bcast = 0;
+      if (a.lhs.mode != M_FULL && a.rhs.mode == M_FULL) std::swap(a.lhs, a.rhs);  // dot commutes
+      int mp = MP_GEN;
+      if (F == 4 && a.lhs.mode == M_FULL)
+        mp = a.rhs.mode == M_FULL ? MP_FF : (a.rhs.mode == M_HOIST ? MP_FH : MP_GEN);
+      a.need_eid = (a.lhs.from_eid && a.lhs.mode != M_HOIST) ||
+                   (a.rhs.from_eid && a.rhs.mode != M_HOIST);
+      a.Z = Z; a.ldz = ldz; a.counts = counts;
+      e = launch_spmm_rows_dot_sum(F == 8, Vd, mp, a, a.blocks_per_tile, s);
+      g_launches++;
+      return cuda_status(e, "gmp_gspmm(dot rows)");
+    }
     SpmmDotArgs a{};
     a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
     a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.dim = dim;

@@ -83,7 +83,7 @@ template <int OP>
 __device__ __forceinline__ double apply_op(double a, double b) {
   if constexpr (OP == OP_ADD) return a + b;
   else if constexpr (OP == OP_SUB) return a - b;
-  else if constexpr (OP == OP_MUL) return a * b;
+  else if constexpr (OP == OP_MUL || OP == OP_DOT) return a * b;  // dot: one product term
   else if constexpr (OP == OP_DIV) return a / b;  // IEEE division (no fast-math)
   else return a;                                  // OP_COPY
 }

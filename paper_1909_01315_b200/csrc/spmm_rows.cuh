@@ -177,7 +177,7 @@ struct RowAcc {
           const float2 x = f2((float)a[k], (float)a[k + 1]);
           if constexpr (OP == OP_COPY) {
             two_sum2(S, C, x);
-          } else if constexpr (OP == OP_MUL) {
+          } else if constexpr (OP == OP_MUL || OP == OP_DOT) {
             const float2 y = f2((float)b[k], (float)b[k + 1]);
             const float2 pr = __fmul2_rn(x, y);
             two_sum2(S, C, pr);
@@ -593,6 +593,21 @@ __device__ __forceinline__ void spmm_accumulate_slot(const SpmmArgs& a, int64_t 
 template <typename T, int OP, int RHO, int V>
 __device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_t deg, int col,
                                           bool valid, const RowAcc<T, OP, RHO, V>& acc) {
+  if constexpr (OP == OP_DOT) {
+    // dot message, sum/mean: the row sum of products over every column the
+    // lane group covers (one tile), reduced across the group's lanes
+    double v = 0.0;
+    if (valid)
+#pragma unroll
+      for (int k = 0; k < V; ++k) v += acc.acc[k];
+    const unsigned mask = __activemask();
+    for (int off = 1; off < (1 << a.g_log2); off <<= 1) v += __shfl_xor_sync(mask, v, off);
+    if ((threadIdx.x & ((1 << a.g_log2) - 1)) == 0) {
+      if (a.mean && deg > 0) v = v / (double)deg;
+      static_cast<T*>(a.Z)[row * a.ldz] = (T)v;
+    }
+    return;
+  }
   if (!valid) return;
   T* z = static_cast<T*>(a.Z) + row * a.ldz;
   T out[V];
@@ -771,7 +786,7 @@ cudaError_t launch_spmm_rows_mp(int mp, const SpmmArgs& a, int64_t grid, cudaStr
   if constexpr (sizeof(T) == 4) {
     if constexpr (OP == OP_COPY) {
       if (mp == MP_F) return launch_spmm_rows_t<T, OP, RHO, V, MP_F>(a, grid, s);
-    } else if constexpr (OP != OP_DIV) {
+    } else if constexpr (OP != OP_DIV) {  // add / sub / mul / dot
       if (mp == MP_FF) return launch_spmm_rows_t<T, OP, RHO, V, MP_FF>(a, grid, s);
       if (mp == MP_FS) return launch_spmm_rows_t<T, OP, RHO, V, MP_FS>(a, grid, s);
       if (mp == MP_FH) return launch_spmm_rows_t<T, OP, RHO, V, MP_FH>(a, grid, s);
@@ -788,6 +803,10 @@ cudaError_t launch_spmm_rows_v(int V, int mp, const SpmmArgs& a, int64_t grid, c
   if (V == 2) return launch_spmm_rows_mp<T, OP, RHO, 2>(mp, a, grid, s);
   return launch_spmm_rows_mp<T, OP, RHO, 1>(mp, a, grid, s);
 }
+
+// dot messages under sum/mean (single column tile): spmm_op_dot.cu
+cudaError_t launch_spmm_rows_dot_sum(int dtype_is_f64, int V, int mp, const SpmmArgs& a,
+                                     int64_t grid, cudaStream_t s);
 
 // Instantiated once per OP in spmm_op_<op>.cu so the op families compile in
 // parallel.
