@@ -158,7 +158,7 @@ struct RowAcc {
         const float x = (float)a[0], y = (float)b[0];
         if constexpr (OP == OP_COPY) {
           two_sum1(s[0], c[0], x);
-        } else if constexpr (OP == OP_MUL) {
+        } else if constexpr (OP == OP_MUL || OP == OP_DOT) {
           const float pr = __fmul_rn(x, y);
           two_sum1(s[0], c[0], pr);
           c[0] = __fadd_rn(c[0], __fmaf_rn(x, y, -pr));
