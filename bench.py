@@ -444,6 +444,9 @@ def run_extras(G, kernels, layers, g, X, n, m, flush, stream, dev, args):
     sage = layers.SAGEModel([F, HIDDEN, CLASSES], seed=0, device=dev)
     out["sage_epoch_ms"] = round(_time(lambda: layers.train_epoch(g, X, labels, sage, 0.01),
                                        stream, flush, reps=3), 3)
+    gat = layers.GATModel([F, HIDDEN, HIDDEN, CLASSES], heads=1, seed=0, device=dev)
+    out["gat_epoch_ms"] = round(_time(lambda: layers.train_epoch(g, X, labels, gat, 0.01),
+                                      stream, flush, reps=3), 3)
     return out
 
 

@@ -11,7 +11,9 @@ they own no kernels. Semantics follow /root/reference/pkg/src/graphmp/layers.py:
 Dense projections are torch matmuls (cuBLAS; fp32 with TF32 off by default so
 parity tests compare against the reference's float64 numbers).
 The GAT head scores are computed for all heads in one u_add_v g-SDDMM and
-one fused edge_softmax over (m, H); the per-head u_mul_e aggregations read
+one fused edge_softmax over (m, H); el / er come from X (W a) without the
+projection; the u_mul_e aggregation runs on the narrower of the input and
+the projected features (linearity: sum alpha (X W) = (sum alpha X) W), reading
 strided column views of the (n, H*D) projection, so no head copy is made.
 """
 
@@ -109,17 +111,25 @@ def gat_layer(g, X, params, num_heads=None, **kw):
     Wcat = torch.cat([_t(h.W, dev, dt) for h in heads], dim=1)           # (d_in, H*D)
     D = _t(heads[0].W, dev, dt).shape[1]
     H = len(heads)
-    proj = X @ Wcat                                                       # (n, H*D)
-    pv = proj.view(-1, H, D)
+    d_in = X.shape[1]
     al = torch.stack([_t(h.a_l, dev, dt)[:, 0] for h in heads])           # (H, D)
     ar = torch.stack([_t(h.a_r, dev, dt)[:, 0] for h in heads])
-    el = (pv * al).sum(-1)                                                # (n, H)
-    er = (pv * ar).sum(-1)
+    # el = proj . a_l = X (W a_l): only (d_in, H) extra weights, no projection needed
+    Wv = Wcat.view(d_in, H, D)
+    el = X @ (Wv * al).sum(-1)                                            # (n, H)
+    er = X @ (Wv * ar).sum(-1)
     score = autodiff.gsddmm(g, kernels.add("src", "dst"), X=el, Y=er, **kw)   # (m, H)
     alpha = autodiff.edge_softmax(g, score)
-    outs = [autodiff.gspmm(g, kernels.mul("src", "edge"), "sum",
-                           X=proj[:, h * D:(h + 1) * D], W=alpha[:, h:h + 1], **kw)
-            for h in range(H)]
+    if d_in < D:
+        # sum_u alpha_uv (X_u W) = (sum_u alpha_uv X_u) W: aggregate the narrower
+        # side (same result up to rounding; the reference projects first)
+        outs = [autodiff.gspmm(g, kernels.mul("src", "edge"), "sum", X=X,
+                               W=alpha[:, h:h + 1], **kw) @ Wv[:, h, :] for h in range(H)]
+    else:
+        proj = X @ Wcat                                                   # (n, H*D)
+        outs = [autodiff.gspmm(g, kernels.mul("src", "edge"), "sum",
+                               X=proj[:, h * D:(h + 1) * D], W=alpha[:, h:h + 1], **kw)
+                for h in range(H)]
     return outs[0] if H == 1 else torch.cat(outs, dim=1)
 
 
@@ -190,6 +200,38 @@ class SAGEModel:
         last = len(self.layers) - 1
         for i, p in enumerate(self.layers):
             h = sage_layer(g, h, p, act="relu" if i < last else "linear", **kw)
+        return h
+
+
+class GATModel:
+    """Stack of GAT layers (heads concatenated, relu between layers, linear
+    last) - the Reddit GAT epoch of the paper is 3 layers x 16 hidden x 1 head
+    (PAPER.md:965-966); the reference only defines the single gat_layer."""
+
+    def __init__(self, dims, heads=1, seed=0, device=None, dtype=torch.float32):
+        rng = np.random.default_rng(seed)
+        device = device or default_device()
+        self.layers = []
+        d_in = dims[0]
+        for i, d_out in enumerate(dims[1:]):
+            last = i == len(dims) - 2
+            h = 1 if last else heads
+            p = init_gat(rng, d_in, d_out if last else d_out // h, h)
+            for hp in p.heads:
+                hp.W, hp.a_l, hp.a_r = (_leaf(a, device, dtype) for a in (hp.W, hp.a_l, hp.a_r))
+            self.layers.append(p)
+            d_in = d_out
+
+    def parameters(self):
+        return [t for p in self.layers for hp in p.heads for t in (hp.W, hp.a_l, hp.a_r)]
+
+    def forward(self, g, x, **kw):
+        h = x
+        last = len(self.layers) - 1
+        for i, p in enumerate(self.layers):
+            h = gat_layer(g, h, p, **kw)
+            if i < last:
+                h = torch.relu(h)
         return h
 
 

@@ -80,6 +80,10 @@ def main():
         labels = torch.randint(0, 41, (n,), generator=gen, device=dev)
         model = layers.GCNModel([F, 16, 41], seed=0, device=dev)
         ops["gcn_epoch"] = lambda: layers.train_epoch(g, X, labels, model, 0.01)
+    if a.op == "gat_epoch":
+        labels = torch.randint(0, 41, (n,), generator=gen, device=dev)
+        model = layers.GATModel([F, 16, 16, 41], heads=1, seed=0, device=dev)
+        ops["gat_epoch"] = lambda: layers.train_epoch(g, X, labels, model, 0.01)
     fn = ops[a.op]
     ctx = kernels.tuning(tile_cols=a.tile_cols or None, l2_budget_mb=a.l2mb or None)
     with ctx:
