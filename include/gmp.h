@@ -160,6 +160,15 @@ int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sc
                          void* alpha, int64_t lda, void* workspace, size_t workspace_bytes,
                          void* stream);
 
+/* Fused u_add_v scores + edge_softmax (GAT attention, layers.py:110-113):
+ * alpha = edge_softmax(s) with s[e,h] = el[src e, h] + er[dst e, h] computed
+ * on the fly - the (m, H) score matrix is never written or re-read.
+ * el, er: (n, H) node-keyed, leading dims lde / ldr. */
+int gmp_edge_softmax_uv_fwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sched* sched,
+                            int dtype, const void* el, int64_t lde, const void* er, int64_t ldr,
+                            int32_t H, void* alpha, int64_t lda, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
 /* Fused backward of edge_softmax (the composition of the four kernel
  * backwards of messaging.py:117-121, autodiff.py:398-418):
  *   ds[e,h] = alpha[e,h] * (g[e,h] - sum_{e'->v} alpha[e',h] g[e',h]) */

@@ -20,7 +20,7 @@ RHOS = {"sum": 0, "max": 1, "min": 2, "mean": 3}
 GMP_F32, GMP_F64 = 0, 1
 
 EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "gmp_gsddmm",
-            "gmp_edge_softmax_workspace_size", "gmp_edge_softmax_fwd", "gmp_edge_softmax_bwd", "gmp_route_extrema",
+            "gmp_edge_softmax_workspace_size", "gmp_edge_softmax_fwd", "gmp_edge_softmax_uv_fwd", "gmp_edge_softmax_bwd", "gmp_route_extrema",
             "gmp_extrema_bwd_copy", "gmp_gather_rows", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
             "gmp_version")
 
@@ -77,6 +77,8 @@ def _declare(lib):
     lib.gmp_edge_softmax_workspace_size.restype = ctypes.c_size_t
     lib.gmp_edge_softmax_fwd.argtypes = [_P(GmpAdj), _P(GmpCoo), _P(GmpSched), c_int, vp, i64, i32,
                                          vp, i64, vp, ctypes.c_size_t, vp]
+    lib.gmp_edge_softmax_uv_fwd.argtypes = [_P(GmpAdj), _P(GmpCoo), _P(GmpSched), c_int, vp, i64,
+                                            vp, i64, i32, vp, i64, vp, ctypes.c_size_t, vp]
     lib.gmp_edge_softmax_bwd.argtypes = [_P(GmpAdj), _P(GmpCoo), _P(GmpSched), c_int, vp, i64, vp,
                                          i64, i32, vp, i64, vp, ctypes.c_size_t, vp]
     lib.gmp_route_extrema.argtypes = [i64, i32, c_int, vp, vp, i64, vp, i64, vp]
@@ -87,6 +89,7 @@ def _declare(lib):
     lib.gmp_strerror.restype = ctypes.c_char_p
     lib.gmp_launch_count.restype = ctypes.c_uint64
     for name in ("gmp_build_schedule", "gmp_gspmm", "gmp_gsddmm", "gmp_edge_softmax_fwd",
+                 "gmp_edge_softmax_uv_fwd",
                  "gmp_edge_softmax_bwd", "gmp_route_extrema", "gmp_extrema_bwd_copy",
                  "gmp_gather_rows", "gmp_version"):
         getattr(lib, name).restype = c_int

@@ -267,6 +267,34 @@ class _EdgeSoftmax(torch.autograd.Function):
         return None, _match(ds, ctx.like)
 
 
+class _EdgeSoftmaxUV(torch.autograd.Function):
+    """alpha = edge_softmax(u_add_v(el, er)); backward = fused softmax backward
+    then the u_add_v g-SDDMM backward (Theorem 1: d el on reverse(g), d er on g)."""
+
+    @staticmethod
+    def forward(ctx, g, el, er):
+        alpha = kernels.edge_softmax_uv_forward(g, el, er)
+        ctx.g = g
+        ctx.save_for_backward(alpha, el, er)
+        return alpha
+
+    @staticmethod
+    def backward(ctx, grad):
+        alpha, el, er = ctx.saved_tensors
+        ds = kernels.edge_softmax_backward(ctx.g, alpha, grad.contiguous())
+        needs = tuple(k for k, need in (("x", ctx.needs_input_grad[1]),
+                                        ("y", ctx.needs_input_grad[2])) if need)
+        b = gsddmm_backward(ctx.g, kernels.add("src", "dst"), X=el, Y=er, dM=ds, needs=needs)
+        return None, _match(b.dx, el), _match(b.dy, er)
+
+
+def edge_softmax_uv(g, el, er):
+    """Differentiable edge_softmax of u_add_v(el, er), scores never materialised."""
+    if _grad_enabled(el, er):
+        return _EdgeSoftmaxUV.apply(g, el, er)
+    return kernels.edge_softmax_uv_forward(g, el, er)
+
+
 def _grad_enabled(*xs):
     return torch.is_grad_enabled() and any(torch.is_tensor(x) and x.requires_grad for x in xs)
 

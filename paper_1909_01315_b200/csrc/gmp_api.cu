@@ -431,21 +431,26 @@ size_t gmp_edge_softmax_workspace_size(int64_t n_rows, int32_t H) {
 static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sched* sched,
                           int dtype, const void* s, int64_t lds, const void* g, int64_t ldg,
                           int32_t H, void* out, int64_t ldo, void* ws, size_t ws_bytes, bool bwd,
-                          void* stream) {
+                          void* stream, const void* el = nullptr, int64_t lde = 0,
+                          const void* er = nullptr, int64_t ldr = 0) {
+  const bool uv = el != nullptr;
   if (!adj || !coo) return fail(GMP_EINVAL, "null adjacency or coo");
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
   if (adj->m < 0 || adj->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
   if (coo->m != adj->m) return fail(GMP_EINVAL, "coo and adjacency edge counts differ");
-  if (H < 0 || lds < H || ldo < H || (bwd && ldg < H)) return fail(GMP_EINVAL, "bad head count / ld");
+  if (H < 0 || (!uv && lds < H) || ldo < H || (bwd && ldg < H) || (uv && (lde < H || ldr < H || !er)))
+    return fail(GMP_EINVAL, "bad head count / ld");
   if (adj->m == 0 || H == 0 || adj->n_rows == 0) return GMP_OK;
-  if (!s || !out || (bwd && !g) || !adj->eids || !adj->indptr || !coo->dst)
+  if ((!s && !uv) || !out || (bwd && !g) || !adj->eids || !adj->indptr || !coo->dst ||
+      (uv && (!adj->indices || !coo->src)))
     return fail(GMP_EINVAL, "null arrays");
   if (!ws || ws_bytes < gmp_edge_softmax_workspace_size(adj->n_rows, H))
     return fail(GMP_EINVAL, "softmax workspace too small");
   const size_t F = dtype == GMP_F64 ? 8 : 4;
   Opnd ops[2] = {};
-  ops[0].present = true; ops[0].dev.data = s; ops[0].dev.ld = lds;
+  ops[0].present = true; ops[0].dev.data = uv ? el : s; ops[0].dev.ld = uv ? lde : lds;
   if (bwd) { ops[1].present = true; ops[1].dev.data = g; ops[1].dev.ld = ldg; }
+  if (uv) { ops[1].present = true; ops[1].dev.data = er; ops[1].dev.ld = ldr; }
   const int V = pick_v(F, H, ops, 2, out, ldo, nullptr);
   int tw = std::min(H, 32 * V);
   const int ntiles = (H + tw - 1) / tw;
@@ -453,18 +458,19 @@ static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sche
   const int G = std::min(32, next_pow2((tw + V - 1) / V));
   const int64_t n_heavy = sched ? sched->n_heavy : 0;
   SoftmaxArgs a{};
-  a.indptr = adj->indptr; a.eids = adj->eids; a.order = sched ? sched->order : nullptr;
+  a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = sched ? sched->order : nullptr;
   a.n_rows = adj->n_rows; a.n_heavy = n_heavy;
   a.blocks_per_tile = n_heavy + (adj->n_rows - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
   a.H = H; a.tile_cols = tw; a.g_log2 = log2i(G);
   a.s = s; a.lds = lds; a.g = g; a.ldg = ldg; a.out = out; a.ldo = ldo;
   a.dst = coo->dst; a.m = coo->m;
   a.stat = ws;
+  a.el = el; a.lde = lde; a.er = er; a.ldr = ldr; a.src = coo->src;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = launch_edge_softmax(F == 8, V, bwd, a, a.blocks_per_tile * ntiles, st);
+  cudaError_t e = launch_edge_softmax(F == 8, V, bwd, uv, a, a.blocks_per_tile * ntiles, st);
   g_launches++;
   if (e == cudaSuccess) {
-    e = launch_edge_softmax_apply(F == 8, V, bwd, a, st);
+    e = launch_edge_softmax_apply(F == 8, V, bwd, uv, a, st);
     g_launches++;
   }
   return cuda_status(e, bwd ? "gmp_edge_softmax_bwd" : "gmp_edge_softmax_fwd");
@@ -475,6 +481,15 @@ int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sc
                          int64_t lda, void* workspace, size_t workspace_bytes, void* stream) {
   return softmax_common(in_adj, coo, sched, dtype, scores, lds, nullptr, 0, H, alpha, lda,
                         workspace, workspace_bytes, false, stream);
+}
+
+int gmp_edge_softmax_uv_fwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sched* sched,
+                            int dtype, const void* el, int64_t lde, const void* er, int64_t ldr,
+                            int32_t H, void* alpha, int64_t lda, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  if (!el || !er) return fail(GMP_EINVAL, "null el / er");
+  return softmax_common(in_adj, coo, sched, dtype, nullptr, 0, nullptr, 0, H, alpha, lda,
+                        workspace, workspace_bytes, false, stream, el, lde, er, ldr);
 }
 
 int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sched* sched,

@@ -61,46 +61,51 @@ cudaError_t launch_sddmm(int f64, int op, int V, const SddmmArgs& a, int64_t gri
   return cudaGetLastError();
 }
 
-template <typename T, bool BWD>
+template <typename T, bool BWD, bool UV>
 static void softmax_v(int V, const SoftmaxArgs& a, int64_t grid, cudaStream_t s) {
   if constexpr (sizeof(T) == 4) {
-    if (V == 4) { edge_softmax_kernel<T, 4, BWD><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a); return; }
+    if (V == 4) { edge_softmax_kernel<T, 4, BWD, UV><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a); return; }
   }
-  if (V == 2) { edge_softmax_kernel<T, 2, BWD><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a); return; }
-  edge_softmax_kernel<T, 1, BWD><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
+  if (V == 2) { edge_softmax_kernel<T, 2, BWD, UV><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a); return; }
+  edge_softmax_kernel<T, 1, BWD, UV><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
 }
 
-cudaError_t launch_edge_softmax(int f64, int V, bool bwd, const SoftmaxArgs& a, int64_t grid,
-                                cudaStream_t s) {
+cudaError_t launch_edge_softmax(int f64, int V, bool bwd, bool uv, const SoftmaxArgs& a,
+                                int64_t grid, cudaStream_t s) {
   if (f64) {
-    if (bwd) softmax_v<double, true>(V, a, grid, s);
-    else softmax_v<double, false>(V, a, grid, s);
+    if (bwd) softmax_v<double, true, false>(V, a, grid, s);
+    else if (uv) softmax_v<double, false, true>(V, a, grid, s);
+    else softmax_v<double, false, false>(V, a, grid, s);
   } else {
-    if (bwd) softmax_v<float, true>(V, a, grid, s);
-    else softmax_v<float, false>(V, a, grid, s);
+    if (bwd) softmax_v<float, true, false>(V, a, grid, s);
+    else if (uv) softmax_v<float, false, true>(V, a, grid, s);
+    else softmax_v<float, false, false>(V, a, grid, s);
   }
   return cudaGetLastError();
 }
 
-template <typename T, bool BWD>
+template <typename T, bool BWD, bool UV>
 static void softmax_apply_v(int V, const SoftmaxArgs& a, cudaStream_t s) {
   const int64_t total = a.m * (int64_t)(a.H / V);
   const unsigned grid = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>((total + 256 * kApplyU - 1) / (256 * kApplyU), 148 * 64));
   if constexpr (sizeof(T) == 4) {
-    if (V == 4) { edge_softmax_apply_kernel<T, 4, BWD><<<grid, 256, 0, s>>>(a); return; }
+    if (V == 4) { edge_softmax_apply_kernel<T, 4, BWD, UV><<<grid, 256, 0, s>>>(a); return; }
   }
-  if (V == 2) { edge_softmax_apply_kernel<T, 2, BWD><<<grid, 256, 0, s>>>(a); return; }
-  edge_softmax_apply_kernel<T, 1, BWD><<<grid, 256, 0, s>>>(a);
+  if (V == 2) { edge_softmax_apply_kernel<T, 2, BWD, UV><<<grid, 256, 0, s>>>(a); return; }
+  edge_softmax_apply_kernel<T, 1, BWD, UV><<<grid, 256, 0, s>>>(a);
 }
 
-cudaError_t launch_edge_softmax_apply(int f64, int V, bool bwd, const SoftmaxArgs& a, cudaStream_t s) {
+cudaError_t launch_edge_softmax_apply(int f64, int V, bool bwd, bool uv, const SoftmaxArgs& a,
+                                      cudaStream_t s) {
   if (f64) {
-    if (bwd) softmax_apply_v<double, true>(V, a, s);
-    else softmax_apply_v<double, false>(V, a, s);
+    if (bwd) softmax_apply_v<double, true, false>(V, a, s);
+    else if (uv) softmax_apply_v<double, false, true>(V, a, s);
+    else softmax_apply_v<double, false, false>(V, a, s);
   } else {
-    if (bwd) softmax_apply_v<float, true>(V, a, s);
-    else softmax_apply_v<float, false>(V, a, s);
+    if (bwd) softmax_apply_v<float, true, false>(V, a, s);
+    else if (uv) softmax_apply_v<float, false, true>(V, a, s);
+    else softmax_apply_v<float, false, false>(V, a, s);
   }
   return cudaGetLastError();
 }

@@ -31,6 +31,7 @@ namespace gmp {
 
 struct SoftmaxArgs {
   const int64_t* indptr;
+  const int32_t* indices;
   const int32_t* eids;
   const int32_t* order;
   int64_t n_rows;
@@ -48,6 +49,13 @@ struct SoftmaxArgs {
   const int32_t* dst;  // COO destinations (apply kernel)
   int64_t m;
   void* stat;          // (n_rows, 2H) of T: [max | 1/sum] fwd, [sum_hi | sum_lo] bwd
+  // fused u_add_v scores (forward only): s[e] = el[src e] + er[dst e], never
+  // materialised (GAT attention logits, layers.py:110-113); null = read s
+  const void* el;
+  int64_t lde;
+  const void* er;
+  int64_t ldr;
+  const int32_t* src;  // COO sources (apply kernel, fused mode)
 };
 
 __device__ __forceinline__ float exp_t(float x) { return expf(x); }
@@ -89,7 +97,7 @@ template <> struct ColSum<double> {
 // one warp step.
 constexpr int kChunk = 256;
 
-template <typename T, int V, bool BWD>
+template <typename T, int V, bool BWD, bool UV>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const SoftmaxArgs a) {
   constexpr int U = V == 4 ? 4 : 8;
   constexpr int B = kChunk / 32;
@@ -119,6 +127,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
   const int ccol = valid ? col : 0;
   const T* S = static_cast<const T*>(a.s) + ccol;
   const T* Gd = static_cast<const T*>(a.g) + ccol;
+  const T* EL = UV ? static_cast<const T*>(a.el) + ccol : nullptr;
+  T er_row[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) er_row[k] = T(0);
+  if (UV) load_vec<T, V>(static_cast<const T*>(a.er) + row * a.ldr + ccol, er_row);
   T* O = static_cast<T*>(a.out) + ccol;
   const int64_t first = heavy ? (int64_t)warp * kChunk : 0;
   const int64_t stride = heavy ? (int64_t)kChunk * kWarpsPerCta : kChunk;
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
 #pragma unroll
     for (int i = 0; i < B; ++i) {
       const int64_t q = cb + i * 32 + lane;
-      pre[i] = q < pe ? __ldg(a.eids + q) : 0;
+      pre[i] = q < pe ? __ldg((UV ? a.indices : a.eids) + q) : 0;
     }
   };
   auto stage = [&]() {
@@ -160,7 +173,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
         const int64_t e = buf[j & (kChunk - 1)];
 #pragma unroll
         for (int k = 0; k < V; ++k) x[u][k] = gg[u][k] = T(0);
-        if (ok[u]) {
+        if (UV && ok[u]) {  // e is the source node: score = el[u] + er[row]
+          load_vec<T, V>(EL + e * a.lde, x[u]);
+#pragma unroll
+          for (int k = 0; k < V; ++k) x[u][k] = x[u][k] + er_row[k];
+        } else if (ok[u]) {
           load_vec<T, V>(S + e * a.lds, x[u]);
           if constexpr (BWD) load_vec<T, V>(Gd + e * a.ldg, gg[u]);
         }
@@ -252,7 +269,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
 // kApplyU independent vectors in flight.
 constexpr int kApplyU = 4;
 
-template <typename T, int V, bool BWD>
+template <typename T, int V, bool BWD, bool UV>
 __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxArgs a) {
   const int per_edge = a.H / V;  // vectors per edge row
   const int64_t total = a.m * (int64_t)per_edge;
@@ -273,7 +290,15 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
       ev[u] = e;
       cv[u] = c;
       const int64_t v = __ldg(a.dst + e);
-      load_vec<T, V>(static_cast<const T*>(a.s) + e * a.lds + c, x[u]);
+      if constexpr (UV) {
+        T xr[V];
+        load_vec<T, V>(static_cast<const T*>(a.el) + (int64_t)__ldg(a.src + e) * a.lde + c, x[u]);
+        load_vec<T, V>(static_cast<const T*>(a.er) + v * a.ldr + c, xr);
+#pragma unroll
+        for (int k = 0; k < V; ++k) x[u][k] = x[u][k] + xr[k];
+      } else {
+        load_vec<T, V>(static_cast<const T*>(a.s) + e * a.lds + c, x[u]);
+      }
       if constexpr (BWD) load_vec<T, V>(static_cast<const T*>(a.g) + e * a.ldg + c, gg[u]);
       // stats row v: [pair0 (H) | pair1 (H)] interleaved as 2*H per row
       load_vec<T, V>(st + v * 2 * a.H + c, p0[u]);
@@ -305,9 +330,9 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
   }
 }
 
-cudaError_t launch_edge_softmax(int dtype_is_f64, int V, bool bwd, const SoftmaxArgs& a,
+cudaError_t launch_edge_softmax(int dtype_is_f64, int V, bool bwd, bool uv, const SoftmaxArgs& a,
                                 int64_t grid, cudaStream_t s);
-cudaError_t launch_edge_softmax_apply(int dtype_is_f64, int V, bool bwd, const SoftmaxArgs& a,
-                                      cudaStream_t s);
+cudaError_t launch_edge_softmax_apply(int dtype_is_f64, int V, bool bwd, bool uv,
+                                      const SoftmaxArgs& a, cudaStream_t s);
 
 }  // namespace gmp

@@ -573,3 +573,32 @@ def edge_softmax_backward(g, alpha, grad):
     if ds.numel():
         _softmax_call(g, "gmp_edge_softmax_bwd", A, Gr, H, ds, "gmp_edge_softmax_bwd")
     return ds
+
+
+def edge_softmax_uv_forward(g, el, er):
+    """alpha = edge_softmax(el[src] + er[dst]) without materialising the
+    scores (fused u_add_v g-SDDMM + edge_softmax, GAT layers.py:110-113)."""
+    _require_cuda(g)
+    L = _as_matrix("el", el, g.num_nodes, g.device)
+    R = _as_matrix("er", er, g.num_nodes, g.device)
+    if L.dtype != R.dtype:
+        L, R = L.to(torch.float64), R.to(torch.float64)
+    if L.shape[1] != R.shape[1]:
+        raise ValueError("el and er need the same head count, got %d and %d"
+                         % (L.shape[1], R.shape[1]))
+    H = L.shape[1]
+    accounting.log_dispatch("gspmm", g.uid, "edge_softmax(add(src,dst))", "softmax",
+                            "node_parallel", g.num_edges, H)
+    alpha = accounting.register(torch.empty((g.num_edges, H), dtype=L.dtype, device=g.device))
+    if alpha.numel():
+        lib = _lib.load()
+        adj = g.to_csc()
+        sched = adj.schedule()
+        ws_bytes = int(lib.gmp_edge_softmax_workspace_size(g.num_nodes, H))
+        ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=g.device)
+        coo = _lib.GmpCoo(g.num_nodes, g.num_edges, g.src.data_ptr(), g.dst.data_ptr())
+        _lib.check(lib.gmp_edge_softmax_uv_fwd(
+            ctypes.byref(_adj_struct(adj)), ctypes.byref(coo), ctypes.byref(sched.struct),
+            _dtype_code(L), L.data_ptr(), _ld(L), R.data_ptr(), _ld(R), H, alpha.data_ptr(), H,
+            ws.data_ptr(), ws_bytes, _stream(g.device)), "gmp_edge_softmax_uv_fwd")
+    return alpha

@@ -10,8 +10,8 @@ they own no kernels. Semantics follow /root/reference/pkg/src/graphmp/layers.py:
 `aggregator="sum"` gives the copy_u+sum GCN named by BASELINE.json config 0.
 Dense projections are torch matmuls (cuBLAS; fp32 with TF32 off by default so
 parity tests compare against the reference's float64 numbers).
-The GAT head scores are computed for all heads in one u_add_v g-SDDMM and
-one fused edge_softmax over (m, H); el / er come from X (W a) without the
+The GAT head scores (u_add_v) and edge_softmax run as one fused kernel pair
+over (m, H) that never stores the scores; el / er come from X (W a) without the
 projection; the u_mul_e aggregation runs on the narrower of the input and
 the projected features (linearity: sum alpha (X W) = (sum alpha X) W), reading
 strided column views of the (n, H*D) projection, so no head copy is made.
@@ -118,8 +118,8 @@ def gat_layer(g, X, params, num_heads=None, **kw):
     Wv = Wcat.view(d_in, H, D)
     el = X @ (Wv * al).sum(-1)                                            # (n, H)
     er = X @ (Wv * ar).sum(-1)
-    score = autodiff.gsddmm(g, kernels.add("src", "dst"), X=el, Y=er, **kw)   # (m, H)
-    alpha = autodiff.edge_softmax(g, score)
+    # u_add_v scores + edge_softmax fused: the (m, H) scores are never stored
+    alpha = autodiff.edge_softmax_uv(g, el.contiguous(), er.contiguous())  # (m, H)
     if d_in < D:
         # sum_u alpha_uv (X_u W) = (sum_u alpha_uv X_u) W: aggregate the narrower
         # side (same result up to rounding; the reference projects first)

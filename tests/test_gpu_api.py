@@ -229,3 +229,26 @@ def test_two_process_row_partition_on_gpu():
         assert rel_err(z, want[r0:r1]) < 1e-12
         assert rel_err(z_ov, want[r0:r1]) < 1e-12
         assert rel_err(dx, want_dx[r0:r1]) < 1e-12
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_fused_uv_softmax_matches_composition(dtype):
+    """edge_softmax(u_add_v(el, er)) fused == gsddmm(add) then edge_softmax,
+    forward bit-identical (same fp32 score rounding) and gradients equal."""
+    s, d = G.generators.power_law_edges(5000, 10, seed=2)
+    g = G.from_arrays(s, d, num_nodes=5000, device=DEV)
+    for H in (1, 3, 8):
+        el = torch.randn(5000, H, device=DEV, dtype=dtype).requires_grad_(True)
+        er = torch.randn(5000, H, device=DEV, dtype=dtype).requires_grad_(True)
+        u = torch.randn(g.num_edges, H, device=DEV, dtype=dtype)
+        a1 = G.autodiff.edge_softmax_uv(g, el, er)
+        (a1 * u).sum().backward()
+        g1 = (el.grad.clone(), er.grad.clone())
+        el.grad = er.grad = None
+        score = G.autodiff.gsddmm(g, kernels.add("src", "dst"), X=el, Y=er)
+        a2 = G.edge_softmax(g, score)
+        (a2 * u).sum().backward()
+        assert torch.equal(a1, a2), H
+        tol = 1e-12 if dtype == torch.float64 else 1e-5
+        assert rel_err(to_np(g1[0]), to_np(el.grad)) < tol
+        assert rel_err(to_np(g1[1]), to_np(er.grad)) < tol
