@@ -252,3 +252,17 @@ def test_fused_uv_softmax_matches_composition(dtype):
         tol = 1e-12 if dtype == torch.float64 else 1e-5
         assert rel_err(to_np(g1[0]), to_np(el.grad)) < tol
         assert rel_err(to_np(g1[1]), to_np(er.grad)) < tol
+
+
+def test_host_pipeline_matches_device_gspmm():
+    from paper_1909_01315_b200 import pipeline
+    s, d = G.generators.power_law_edges(20000, 30, seed=4)
+    g = G.from_arrays(s, d, num_nodes=20000, device=DEV)
+    for F in (62, 130, 602):
+        x = torch.randn(20000, F, dtype=torch.float32).pin_memory()
+        z = torch.empty(20000, F, dtype=torch.float32).pin_memory()
+        for rho in ("sum", "mean"):
+            pipeline.gspmm_host(g, x, z, rho)
+            torch.cuda.synchronize()
+            want, _ = G.gspmm(g, kernels.copy("src"), rho, X=x.to(DEV))
+            assert torch.equal(z, want.cpu()), (F, rho)
