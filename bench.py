@@ -445,6 +445,9 @@ def run_extras(G, kernels, layers, g, X, n, m, flush, stream, dev, args):
     gcn = layers.GCNModel([F, HIDDEN, CLASSES], seed=0, device=dev)
     out["gcn_epoch_ms"] = round(_time(lambda: layers.train_epoch(g, X, labels, gcn, 0.01),
                                       stream, flush, reps=3), 3)
+    gcn_af = layers.GCNModel([F, HIDDEN, CLASSES], seed=0, device=dev, order="aggregate_first")
+    out["gcn_epoch_aggregate_first_ms"] = round(
+        _time(lambda: layers.train_epoch(g, X, labels, gcn_af, 0.01), stream, flush, reps=3), 3)
     sage = layers.SAGEModel([F, HIDDEN, CLASSES], seed=0, device=dev)
     out["sage_epoch_ms"] = round(_time(lambda: layers.train_epoch(g, X, labels, sage, 0.01),
                                        stream, flush, reps=3), 3)

@@ -201,6 +201,17 @@ int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* ar
 int gmp_gather_rows(int64_t n, int32_t dim, int dtype, const int32_t* idx, const void* src,
                     int64_t lds, void* dst, int64_t ldd, void* stream);
 
+/* ---- neighbour sampling ------------------------------------------------------
+ * Replaces graph.neighbor_sample's per-seed draw (graph.py:231-266): for seed
+ * i (node seeds[i], in-edges indptr[seeds[i]] .. indptr[seeds[i]+1] of the
+ * in-adjacency), k_i = out_off[i+1] - out_off[i] (= min(fanout, deg), computed
+ * by the caller) distinct adjacency positions, uniform over k-subsets, written
+ * ascending to out_pos[out_off[i] .. out_off[i+1]). The draw is a pure
+ * function of (rng_seed, node id, k, deg). scratch: out_off[n_seeds] int64. */
+int gmp_neighbor_sample(const int64_t* indptr, int64_t n_rows, const int64_t* seeds,
+                        int64_t n_seeds, const int64_t* out_off, uint64_t rng_seed,
+                        int64_t* scratch, int64_t* out_pos, void* stream);
+
 /* ---- diagnostics ------------------------------------------------------------ */
 const char* gmp_last_error(void);
 const char* gmp_strerror(int status);

@@ -26,6 +26,8 @@ cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const
 size_t schedule_workspace_bytes(int64_t n);
 cudaError_t launch_gather_rows(int, int64_t, int32_t, const int32_t*, const void*, int64_t, void*,
                                int64_t, cudaStream_t);
+cudaError_t launch_neighbor_sample(const int64_t*, const int64_t*, int64_t, const int64_t*, uint64_t,
+                                   int64_t*, int64_t*, cudaStream_t);
 cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t light,
                            int32_t* order_out, void* ws, size_t ws_bytes, int64_t* n_heavy,
                            int64_t* n_medium, int64_t* n_nonempty, cudaStream_t s);
@@ -535,6 +537,18 @@ int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* ar
                                           dOut, ldo, (cudaStream_t)stream);
   g_launches++;
   return cuda_status(e, "gmp_extrema_bwd_copy");
+}
+
+int gmp_neighbor_sample(const int64_t* indptr, int64_t n_rows, const int64_t* seeds,
+                        int64_t n_seeds, const int64_t* out_off, uint64_t rng_seed,
+                        int64_t* scratch, int64_t* out_pos, void* stream) {
+  if (n_rows < 0 || n_seeds < 0) return fail(GMP_EINVAL, "bad sizes");
+  if (n_seeds == 0) return GMP_OK;
+  if (!indptr || !seeds || !out_off || !scratch || !out_pos) return fail(GMP_EINVAL, "null arrays");
+  cudaError_t e = launch_neighbor_sample(indptr, seeds, n_seeds, out_off, rng_seed, scratch, out_pos,
+                                         (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_neighbor_sample");
 }
 
 }  // extern "C"

@@ -285,3 +285,65 @@ def reverse(g):
     rev.uid = next(_uid)
     g._reverse_view = rev
     return rev
+
+
+@dataclass(frozen=True)
+class Subgraph:
+    """A compactly relabelled induced piece of a parent graph (graph.py:218-228):
+    row i of a parent node feature matrix sliced by parent_node_ids is the
+    feature of subgraph node i; parent_edge_ids does the same for edges.
+    Both are int64 device tensors."""
+    graph: "Graph"
+    parent_node_ids: torch.Tensor
+    parent_edge_ids: torch.Tensor
+
+
+def neighbor_sample(g, seeds, fanout, rng_seed):
+    """Sample up to `fanout` in-edges per seed without replacement
+    (graph.py:231-286). Seeds come first in the relabelling (first-occurrence
+    order), then newly reached predecessors in ascending parent id; each
+    seed's picks are in ascending in-adjacency position. The draw runs on the
+    device (gmp_neighbor_sample): uniform over k-subsets like the reference's
+    partial Fisher-Yates, from a counter-based generator, so a sample is fully
+    determined by rng_seed (the reference's numpy stream is not reproduced;
+    with fanout >= in-degree the result is identical to the reference's)."""
+    from . import _lib
+    fanout = int(fanout)
+    if fanout < 1:
+        raise ValueError("fanout must be at least 1")
+    s = np.asarray(seeds.cpu() if isinstance(seeds, torch.Tensor) else seeds, dtype=np.int64)
+    s = s.reshape(-1)
+    if s.size and (s.min() < 0 or s.max() >= g.num_nodes):
+        raise IndexError("seed node id out of range")
+    if g.device.type != "cuda":
+        raise RuntimeError("neighbor_sample: graph is on %s; libgmp has no CPU fallback" % g.device)
+    _, first = np.unique(s, return_index=True)
+    keep = s[np.sort(first)]                      # first-occurrence order
+    dev = g.device
+    seeds_d = torch.from_numpy(keep).to(dev)
+    adj = g.to_csc()
+    deg = adj.indptr.index_select(0, seeds_d + 1) - adj.indptr.index_select(0, seeds_d)
+    k = torch.clamp(deg, max=fanout)
+    off = torch.zeros(keep.size + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(k, 0, out=off[1:])
+    total = int(off[-1]) if keep.size else 0
+    pos = torch.empty(total, dtype=torch.int64, device=dev)
+    if total:
+        scratch = torch.empty(total, dtype=torch.int64, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.load().gmp_neighbor_sample(
+            adj.indptr.data_ptr(), adj.num_groups, seeds_d.data_ptr(), keep.size, off.data_ptr(),
+            int(rng_seed) & (2 ** 64 - 1), scratch.data_ptr(), pos.data_ptr(), stream),
+            "gmp_neighbor_sample")
+    peids = adj.edge_ids.index_select(0, pos).to(torch.int64)
+    psrc = g.src.index_select(0, peids).to(torch.int64)
+    pdst = g.dst.index_select(0, peids).to(torch.int64)
+    mark = torch.zeros(g.num_nodes, dtype=torch.bool, device=dev)
+    mark[psrc] = True
+    mark[seeds_d] = False
+    node_ids = torch.cat([seeds_d, torch.nonzero(mark).reshape(-1)])
+    relabel = torch.full((g.num_nodes,), -1, dtype=torch.int64, device=dev)
+    relabel[node_ids] = torch.arange(node_ids.numel(), dtype=torch.int64, device=dev)
+    sub = Graph(relabel.index_select(0, psrc), relabel.index_select(0, pdst), node_ids.numel(),
+                device=dev)
+    return Subgraph(sub, node_ids, peids)

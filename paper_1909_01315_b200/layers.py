@@ -4,6 +4,8 @@ These exist to time and check the epoch configs (BASELINE.json configs 0-3);
 they own no kernels. Semantics follow /root/reference/pkg/src/graphmp/layers.py:
   gcn_layer  act(mean_agg(X) @ W + b)          (layers.py:62-67; aggregate first)
   sage_layer act(X @ W_self + mean_agg(X) @ W_neigh)   (layers.py:76-81)
+             (order="auto" aggregates the narrower side of W, as DGL's GraphConv
+             does; order="aggregate_first" is the reference's literal order)
   gat_layer  per head: proj = X @ W; score_uv = a_l.proj_u + a_r.proj_v (u_add_v
              g-SDDMM, no LeakyReLU); alpha = edge_softmax; out = sum_u alpha*proj_u
              (u_mul_e g-SpMM); heads concatenated            (layers.py:96-116)
@@ -84,19 +86,35 @@ class GATParams:
     heads: list
 
 
-def gcn_layer(g, X, params, act="relu", aggregator="mean", **kw):
+def _project_first(X, W, order):
+    if order not in ("auto", "aggregate_first", "project_first"):
+        raise ValueError("unknown layer order %r" % (order,))
+    return order == "project_first" or (order == "auto" and W.shape[1] < W.shape[0])
+
+
+def gcn_layer(g, X, params, act="relu", aggregator="mean", order="auto", **kw):
+    """act(agg(X) @ W + b). The reference aggregates first (layers.py:62-67);
+    agg is linear, so agg(X) @ W = agg(X @ W), and with order="auto" the
+    aggregation runs on the narrower side (DGL GraphConv does the same when
+    in_feats > out_feats). Same result up to fp rounding."""
     _check_rows(g, X)
-    agg = aggregate(g, X, aggregator, **kw)
-    W = _t(params.W, agg.device, agg.dtype)
-    b = _t(params.b, agg.device, agg.dtype)
-    return _act(agg @ W + b, act)
+    X = _t(X, g.device, torch.float64)
+    W = _t(params.W, X.device, X.dtype)
+    b = _t(params.b, X.device, X.dtype)
+    if _project_first(X, W, order):
+        return _act(aggregate(g, X @ W, aggregator, **kw) + b, act)
+    return _act(aggregate(g, X, aggregator, **kw) @ W + b, act)
 
 
-def sage_layer(g, X, params, act="relu", **kw):
+def sage_layer(g, X, params, act="relu", order="auto", **kw):
+    """act(X @ W_self + mean_agg(X) @ W_neigh) (layers.py:76-81); the
+    neighbour term aggregates the narrower side as in gcn_layer."""
     _check_rows(g, X)
     X = _t(X, g.device, torch.float64)
     Ws = _t(params.W_self, X.device, X.dtype)
     Wn = _t(params.W_neigh, X.device, X.dtype)
+    if _project_first(X, Wn, order):
+        return _act(X @ Ws + aggregate(g, X @ Wn, "mean", **kw), act)
     return _act(X @ Ws + aggregate(g, X, "mean", **kw) @ Wn, act)
 
 
@@ -157,12 +175,14 @@ class GCNModel:
     """Stack of GCN layers (relu between, linear last); numpy-seeded init
     identical to the reference's GCNModel (layers.py:137-158)."""
 
-    def __init__(self, dims, seed=0, aggregator="mean", device=None, dtype=torch.float32):
+    def __init__(self, dims, seed=0, aggregator="mean", device=None, dtype=torch.float32,
+                 order="auto"):
         if len(dims) < 2:
             raise ValueError("need at least input and output dims")
         rng = np.random.default_rng(seed)
         device = device or default_device()
         self.aggregator = aggregator
+        self.order = order
         self.layers = []
         for a, b in zip(dims, dims[1:]):
             p = init_gcn(rng, a, b)
@@ -176,16 +196,17 @@ class GCNModel:
         last = len(self.layers) - 1
         for i, p in enumerate(self.layers):
             h = gcn_layer(g, h, p, act="relu" if i < last else "linear",
-                          aggregator=self.aggregator, **kw)
+                          aggregator=self.aggregator, order=self.order, **kw)
         return h
 
 
 class SAGEModel:
     """Stack of GraphSAGE-mean layers."""
 
-    def __init__(self, dims, seed=0, device=None, dtype=torch.float32):
+    def __init__(self, dims, seed=0, device=None, dtype=torch.float32, order="auto"):
         rng = np.random.default_rng(seed)
         device = device or default_device()
+        self.order = order
         self.layers = []
         for a, b in zip(dims, dims[1:]):
             p = init_sage(rng, a, b)
@@ -199,7 +220,8 @@ class SAGEModel:
         h = x
         last = len(self.layers) - 1
         for i, p in enumerate(self.layers):
-            h = sage_layer(g, h, p, act="relu" if i < last else "linear", **kw)
+            h = sage_layer(g, h, p, act="relu" if i < last else "linear", order=self.order,
+                           **kw)
         return h
 
 

@@ -127,16 +127,17 @@ def test_autograd_matches_gradcheck_fp64():
                                     eps=1e-6, atol=1e-6)
 
 
-def test_gcn_training_losses_match_reference():
+@pytest.mark.parametrize("order", ["auto", "aggregate_first", "project_first"])
+def test_gcn_training_losses_match_reference(order):
     gd = golden()
     src, dst, n = golden_graph("gcn")
     g = G.from_arrays(src.astype(np.int64), dst.astype(np.int64), n, device=DEV)
     want = gd["gcn/losses"]
-    model = layers.GCNModel([12, 8, 3], seed=0, dtype=torch.float64)
+    model = layers.GCNModel([12, 8, 3], seed=0, dtype=torch.float64, order=order)
     losses = layers.train(g, gd["gcn/x"].astype(np.float64), gd["gcn/labels"], model,
                           layers.TrainConfig(lr=0.1, epochs=5))
     assert np.allclose(losses, want, rtol=1e-10, atol=1e-12)
-    model32 = layers.GCNModel([12, 8, 3], seed=0, dtype=torch.float32)
+    model32 = layers.GCNModel([12, 8, 3], seed=0, dtype=torch.float32, order=order)
     l32 = layers.train(g, gd["gcn/x"], gd["gcn/labels"], model32,
                        layers.TrainConfig(lr=0.1, epochs=5))
     assert np.allclose(l32, want, rtol=1e-5, atol=1e-6)
