@@ -177,6 +177,30 @@ int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sc
                          int64_t ldg, int32_t H, void* ds, int64_t ldds, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* Statistics pass alone of the fused u_add_v + edge_softmax: stat (n_rows,
+ * 2H) of the feature dtype receives [max_h | 1/sum_h] per destination row
+ * (rows without in-edges are left untouched). stat_bytes >= n_rows * 2H *
+ * sizeof(element). Consumed by gmp_gat_aggregate. */
+int gmp_edge_softmax_uv_stats(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
+                              const void* el, int64_t lde, const void* er, int64_t ldr, int32_t H,
+                              void* stat, size_t stat_bytes, void* stream);
+
+/* ---- fused GAT attention aggregation -----------------------------------------
+ * One head of the reference's GAT aggregation (layers.py:110-115: u_add_v ->
+ * edge_softmax -> u_mul_e + sum) with the attention weights never stored:
+ *   alpha_e = exp((el[src e] + er[dst e]) - max[dst e]) * inv_sum[dst e]
+ * pack: (n, 4) rows [er, max, inv_sum, 0] (max / inv_sum from
+ * gmp_edge_softmax_uv_stats), el: (n) with stride lde.
+ * backward == 0: adj = in-adjacency, Z[v] = sum_{(u,e)->v} alpha_e X[u]
+ * backward == 1: adj = the reverse graph's in-adjacency (= forward CSR),
+ *                Z[u] = sum_{(v,e): u->v} alpha_e X[v]  (X = upstream grad rows,
+ *                the transposed aggregation of Theorem 1).
+ * X: (n, d) with ldx, Z: (n, d) with ldz. */
+int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int backward,
+                      const void* X, int64_t ldx, int32_t d, const void* el, int64_t lde,
+                      const void* pack, void* Z, int64_t ldz, const gmp_tuning* tuning,
+                      void* stream);
+
 /* ---- extrema gradient routing ----------------------------------------------
  * Replaces kernels.route_extrema_grad (kernels.py:843-857): dM[arg[v,k], k] =
  * dZ[v,k] for every cell with arg >= 0. dM (m, d) must be zero-filled by the

@@ -295,6 +295,83 @@ def edge_softmax_uv(g, el, er):
     return kernels.edge_softmax_uv_forward(g, el, er)
 
 
+class _GATAttention(torch.autograd.Function):
+    """All heads of the reference GAT aggregation (layers.py:110-115):
+    out[:, h] = sum_{(u,e)->v} alpha_{e,h} X_h[u], alpha = edge_softmax(el[u] + er[v]),
+    with X_h = X (shared) or the h-th column block of X. The attention weights
+    are recomputed in the row kernels from el / er / per-destination stats
+    and never stored. Backward (Theorem 1 composed by hand):
+      dX_h[u]  = sum_{u->v} alpha_e dZ_h[v]                 (reverse-graph rows)
+      d el[u]  = sum_{u->v} alpha_e (g_e - S_v)  with g_e = dZ_h[v] . X_h[u],
+                 S_v = sum_{e'->v} alpha_e' g_e' = dZ_h[v] . Z_h[v]
+               = X_h[u] . dX_h[u] - sum_{u->v} alpha_e S_v
+      d er[v]  = S_v (1 - sum_{e->v} alpha_e) = 0   (softmax is shift-invariant)
+    The S_v column rides along the dX aggregation as an extra column."""
+
+    @staticmethod
+    def forward(ctx, g, el, er, X, shared):
+        H = el.shape[1]
+        d = X.shape[1] if shared else X.shape[1] // H
+        stat = kernels.edge_softmax_uv_stats(g, el, er)
+        pack = torch.zeros((H, g.num_nodes, 4), dtype=X.dtype, device=X.device)
+        pack[:, :, 0] = er.t()
+        pack[:, :, 1] = stat[:, :H].t()
+        pack[:, :, 2] = stat[:, H:].t()
+        outs = []
+        for h in range(H):
+            Xh = X if shared else X[:, h * d:(h + 1) * d]
+            outs.append(kernels.gat_aggregate(g, Xh, el[:, h:h + 1], pack[h]))
+        out = outs[0] if H == 1 else torch.cat(outs, dim=1)
+        ctx.g, ctx.shared, ctx.d = g, shared, d
+        ctx.save_for_backward(el, er, X, pack, out)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        el, er, X, pack = ctx.saved_tensors[:4]
+        out = ctx.saved_tensors[4]
+        g, shared, d = ctx.g, ctx.shared, ctx.d
+        H = el.shape[1]
+        dout = dout.to(X.dtype)
+        dp = (d + 1 + 3) // 4 * 4
+        acc = torch.float64
+        dX_parts, del_cols = [], []
+        for h in range(H):
+            dZh = dout[:, h * d:(h + 1) * d]
+            Zh = out[:, h * d:(h + 1) * d]
+            S = (dZh.to(acc) * Zh.to(acc)).sum(1)
+            G2 = torch.zeros((g.num_nodes, dp), dtype=X.dtype, device=X.device)
+            G2[:, :d] = dZh
+            G2[:, d] = S.to(X.dtype)
+            R = kernels.gat_aggregate(g, G2, el[:, h:h + 1], pack[h], backward=True)
+            dXh = R[:, :d]
+            Xh = X if shared else X[:, h * d:(h + 1) * d]
+            del_cols.append(((Xh.to(acc) * dXh.to(acc)).sum(1) - R[:, d].to(acc)).to(X.dtype))
+            dX_parts.append(dXh)
+        if shared:
+            dX = dX_parts[0]
+            for p in dX_parts[1:]:
+                dX = dX + p
+        else:
+            dX = dX_parts[0] if H == 1 else torch.cat(dX_parts, dim=1)
+        dEl = torch.stack(del_cols, dim=1)
+        return None, _match(dEl, el), torch.zeros_like(er), _match(dX, X), None
+
+
+def gat_attention(g, el, er, X, shared=False):
+    """Differentiable fused GAT aggregation of every head (see _GATAttention):
+    (n, H*d) with d = X's width (shared) or X's width / H."""
+    if _grad_enabled(el, er, X):
+        return _GATAttention.apply(g, el, er, X, shared)
+    with torch.no_grad():
+        return _GATAttention.forward(_NoCtx(), g, el, er, X, shared)
+
+
+class _NoCtx:
+    def save_for_backward(self, *a):
+        pass
+
+
 def _grad_enabled(*xs):
     return torch.is_grad_enabled() and any(torch.is_tensor(x) and x.requires_grad for x in xs)
 

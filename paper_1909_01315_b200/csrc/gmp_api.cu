@@ -434,26 +434,27 @@ static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sche
                           int dtype, const void* s, int64_t lds, const void* g, int64_t ldg,
                           int32_t H, void* out, int64_t ldo, void* ws, size_t ws_bytes, bool bwd,
                           void* stream, const void* el = nullptr, int64_t lde = 0,
-                          const void* er = nullptr, int64_t ldr = 0) {
+                          const void* er = nullptr, int64_t ldr = 0, bool stats_only = false) {
   const bool uv = el != nullptr;
-  if (!adj || !coo) return fail(GMP_EINVAL, "null adjacency or coo");
+  if (!adj || (!coo && !stats_only)) return fail(GMP_EINVAL, "null adjacency or coo");
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
   if (adj->m < 0 || adj->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
-  if (coo->m != adj->m) return fail(GMP_EINVAL, "coo and adjacency edge counts differ");
-  if (H < 0 || (!uv && lds < H) || ldo < H || (bwd && ldg < H) || (uv && (lde < H || ldr < H || !er)))
+  if (coo && coo->m != adj->m) return fail(GMP_EINVAL, "coo and adjacency edge counts differ");
+  if (H < 0 || (!uv && lds < H) || (!stats_only && ldo < H) || (bwd && ldg < H) || (uv && (lde < H || ldr < H || !er)))
     return fail(GMP_EINVAL, "bad head count / ld");
   if (adj->m == 0 || H == 0 || adj->n_rows == 0) return GMP_OK;
-  if ((!s && !uv) || !out || (bwd && !g) || !adj->eids || !adj->indptr || !coo->dst ||
-      (uv && (!adj->indices || !coo->src)))
+  if ((!s && !uv) || (!out && !stats_only) || (bwd && !g) || !adj->eids || !adj->indptr ||
+      (!stats_only && !coo->dst) || (uv && (!adj->indices || (!stats_only && !coo->src))))
     return fail(GMP_EINVAL, "null arrays");
-  if (!ws || ws_bytes < gmp_edge_softmax_workspace_size(adj->n_rows, H))
-    return fail(GMP_EINVAL, "softmax workspace too small");
   const size_t F = dtype == GMP_F64 ? 8 : 4;
+  const size_t ws_need = stats_only ? (size_t)adj->n_rows * 2 * (size_t)H * F
+                                    : gmp_edge_softmax_workspace_size(adj->n_rows, H);
+  if (!ws || ws_bytes < ws_need) return fail(GMP_EINVAL, "softmax workspace too small");
   Opnd ops[2] = {};
   ops[0].present = true; ops[0].dev.data = uv ? el : s; ops[0].dev.ld = uv ? lde : lds;
   if (bwd) { ops[1].present = true; ops[1].dev.data = g; ops[1].dev.ld = ldg; }
   if (uv) { ops[1].present = true; ops[1].dev.data = er; ops[1].dev.ld = ldr; }
-  const int V = pick_v(F, H, ops, 2, out, ldo, nullptr);
+  const int V = pick_v(F, H, ops, 2, stats_only ? nullptr : out, ldo, nullptr);
   int tw = std::min(H, 32 * V);
   const int ntiles = (H + tw - 1) / tw;
   tw = ((H + ntiles - 1) / ntiles + V - 1) / V * V;
@@ -465,13 +466,13 @@ static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sche
   a.blocks_per_tile = n_heavy + (adj->n_rows - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
   a.H = H; a.tile_cols = tw; a.g_log2 = log2i(G);
   a.s = s; a.lds = lds; a.g = g; a.ldg = ldg; a.out = out; a.ldo = ldo;
-  a.dst = coo->dst; a.m = coo->m;
+  a.dst = coo ? coo->dst : nullptr; a.m = adj->m;
   a.stat = ws;
-  a.el = el; a.lde = lde; a.er = er; a.ldr = ldr; a.src = coo->src;
+  a.el = el; a.lde = lde; a.er = er; a.ldr = ldr; a.src = coo ? coo->src : nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = launch_edge_softmax(F == 8, V, bwd, uv, a, a.blocks_per_tile * ntiles, st);
   g_launches++;
-  if (e == cudaSuccess) {
+  if (e == cudaSuccess && !stats_only) {
     e = launch_edge_softmax_apply(F == 8, V, bwd, uv, a, st);
     g_launches++;
   }
@@ -537,6 +538,64 @@ int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* ar
                                           dOut, ldo, (cudaStream_t)stream);
   g_launches++;
   return cuda_status(e, "gmp_extrema_bwd_copy");
+}
+
+int gmp_edge_softmax_uv_stats(const gmp_adj* in_adj, const gmp_sched* sched, int dtype,
+                              const void* el, int64_t lde, const void* er, int64_t ldr, int32_t H,
+                              void* stat, size_t stat_bytes, void* stream) {
+  if (!el || !er) return fail(GMP_EINVAL, "null el / er");
+  return softmax_common(in_adj, nullptr, sched, dtype, nullptr, 0, nullptr, 0, H, nullptr, 0, stat,
+                        stat_bytes, false, stream, el, lde, er, ldr, true);
+}
+
+int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int backward,
+                      const void* X, int64_t ldx, int32_t d, const void* el, int64_t lde,
+                      const void* pack, void* Z, int64_t ldz, const gmp_tuning* tuning,
+                      void* stream) {
+  if (!adj) return fail(GMP_EINVAL, "null adjacency");
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (adj->m < 0 || adj->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
+  if (adj->n_rows < 0 || adj->n_rows >= (1ll << 31)) return fail(GMP_EINVAL, "row count out of range");
+  if (d < 0 || ldx < d || ldz < d || lde < 1 || ldx >= (1ll << 32) || lde >= (1ll << 32))
+    return fail(GMP_EINVAL, "bad sizes / leading dimensions");
+  if (adj->n_rows == 0 || d == 0) return GMP_OK;
+  if (!X || !el || !pack || !Z || !adj->indptr || (adj->m > 0 && !adj->indices))
+    return fail(GMP_EINVAL, "null arrays");
+  const size_t F = dtype == GMP_F64 ? 8 : 4;
+  if (!aligned(pack, 4 * F)) return fail(GMP_EINVAL, "pack must be aligned to a 4-element row");
+  if (sched && sched->order == nullptr && sched->n_heavy > 0)
+    return fail(GMP_EINVAL, "schedule has heavy rows but no order");
+  Opnd ops[2] = {};
+  ops[0].present = true; ops[0].dev.data = X; ops[0].dev.ld = ldx; ops[0].dev.dim = d;
+  ops[0].dev.target = GMP_SRC;
+  const int V = pick_v(F, d, ops, 1, Z, ldz, nullptr);
+  const int tw = pick_tile(tuning, d, V, F, adj->n_rows, true, 32 * V);
+  const int G = std::min(32, next_pow2((tw + V - 1) / V));
+  const int ntiles = (d + tw - 1) / tw;
+  const int E = 32 / G;
+  const int64_t n_heavy = sched ? sched->n_heavy : 0;
+  const int32_t* order = sched ? sched->order : nullptr;
+  const bool narrow = (F == 4) && narrow_launch_host(V, log2i(G));
+  const int64_t n_medium = (order && narrow) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
+  const int64_t medium_blocks = (n_medium - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int64_t light_rows = adj->n_rows - n_medium;
+  const int64_t bpt_rows = n_heavy + medium_blocks +
+                           (light_rows + (int64_t)kWarpsPerCta * E - 1) / ((int64_t)kWarpsPerCta * E);
+  SpmmArgs a{};
+  a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
+  a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_medium;
+  a.medium_blocks = medium_blocks; a.blocks_per_tile = bpt_rows;
+  a.d_out = d; a.tile_cols = tw; a.g_log2 = log2i(G); a.mean = 0;
+  a.lhs = row_operand(ops[0]);
+  a.rhs.data = backward ? pack : el; a.rhs.ld = 1; a.rhs.mode = M_SCALAR;
+  a.need_eid = 0;
+  a.Z = Z; a.ldz = ldz;
+  a.attn_el = el; a.attn_lde = (uint32_t)lde; a.attn_pack = pack;
+  const int64_t grid = bpt_rows * ntiles;
+  if (grid >= (1ll << 31)) return fail(GMP_EUNSUPPORTED, "grid too large");
+  cudaError_t e = launch_spmm_rows_attn(F == 8, V, backward != 0, a, grid, (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_gat_aggregate");
 }
 
 int gmp_neighbor_sample(const int64_t* indptr, int64_t n_rows, const int64_t* seeds,

@@ -48,8 +48,20 @@ constexpr int kWarpsPerCta = 8;
 
 // operand access modes inside the row kernel
 enum { M_FULL = 0, M_SCALAR = 1, M_HOIST = 2, M_NONE = 3 };
-// compile-time (lhs, rhs) mode pairs; MP_GEN reads the modes at run time
-enum { MP_F = 0, MP_FF = 1, MP_FS = 2, MP_FH = 3, MP_GEN = 4 };
+// compile-time (lhs, rhs) mode pairs; MP_GEN reads the modes at run time.
+// MP_AF / MP_AB: fused GAT attention (edge_softmax of u_add_v scores times a
+// gathered vector, see gmp_gat_aggregate): lhs is a gathered vector and the
+// per-edge scalar is the attention weight, recomputed from node-keyed data
+//   alpha = exp((el[src] + er[dst]) - max[dst]) * inv_sum[dst]
+// MP_AF walks destination rows (el gathered per edge, (er, max, inv) of the
+// row constant); MP_AB walks source rows of the reverse graph ((er, max, inv)
+// gathered per edge as one packed row, el of the row constant).
+enum { MP_F = 0, MP_FF = 1, MP_FS = 2, MP_FH = 3, MP_GEN = 4, MP_AF = 5, MP_AB = 6 };
+
+template <int MP>
+struct IsAttn {
+  static constexpr bool value = MP == MP_AF || MP == MP_AB;
+};
 
 struct RowOperand {
   const void* data;
@@ -81,7 +93,60 @@ struct SpmmArgs {
   int64_t* arg;
   int64_t* counts;
   int32_t* err_pos;
+  // fused attention (MP_AF / MP_AB only)
+  const void* attn_el;    // (n) el column, stride attn_lde
+  uint32_t attn_lde;
+  const void* attn_pack;  // (n, 4) rows [er, max, inv_sum, 0]
 };
+
+template <typename T>
+__device__ __forceinline__ void load_pack3(const T* p, T& a, T& b, T& c) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    a = v.x; b = v.y; c = v.z;
+  } else {
+    const double2 v0 = __ldg(reinterpret_cast<const double2*>(p));
+    a = v0.x; b = v0.y; c = __ldg(p + 2);
+  }
+}
+
+// row constants of the fused attention: (er, max, inv) of a destination row
+// (MP_AF) or el of a source row (MP_AB, in rc[0])
+template <typename T, int MP>
+__device__ __forceinline__ void attn_row_consts(const SpmmArgs& a, int64_t row, T (&rc)[3]) {
+  rc[0] = rc[1] = rc[2] = T(0);
+  if (row < 0) return;
+  if constexpr (MP == MP_AF) {
+    load_pack3<T>(static_cast<const T*>(a.attn_pack) + row * 4, rc[0], rc[1], rc[2]);
+  } else if constexpr (MP == MP_AB) {
+    rc[0] = __ldg(static_cast<const T*>(a.attn_el) + (uint64_t)row * a.attn_lde);
+  }
+}
+
+__device__ __forceinline__ float attn_exp(float x) { return expf(x); }
+__device__ __forceinline__ double attn_exp(double x) { return exp(x); }
+
+// attention weight of the edge to/from neighbour nb; same fp operation
+// order as the fused softmax (softmax.cuh: s = el + er; exp(s - max) * inv)
+template <typename T, int MP>
+__device__ __forceinline__ T attn_alpha(const SpmmArgs& a, uint32_t nb, const T (&rc)[3]) {
+  if constexpr (MP == MP_AF) {
+    const T x = __ldg(static_cast<const T*>(a.attn_el) + (uint64_t)nb * a.attn_lde) + rc[0];
+    return attn_exp(T(x - rc[1])) * rc[2];
+  } else {
+    T er, mx, inv;
+    load_pack3<T>(static_cast<const T*>(a.attn_pack) + (uint64_t)nb * 4, er, mx, inv);
+    const T x = rc[0] + er;
+    return attn_exp(T(x - mx)) * inv;
+  }
+}
+
+// per-edge scalar operand: a stored scalar, or the recomputed attention weight
+template <typename T, int MP>
+__device__ __forceinline__ T rhs_scalar(const SpmmArgs& a, uint32_t row, const T (&rc)[3]) {
+  if constexpr (IsAttn<MP>::value) return attn_alpha<T, MP>(a, row, rc);
+  else return __ldg(static_cast<const T*>(a.rhs.data) + (uint64_t)row * a.rhs.ld);
+}
 
 // ---- accumulation policies ---------------------------------------------------
 
@@ -278,7 +343,8 @@ template <typename T, int OP, int RHO, int V, int MP, int U>
 __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, int64_t pe,
                                                 int64_t first, int64_t stride, int lane, int slot,
                                                 int E, int col, bool valid, const T (&ha)[V],
-                                                const T (&hb)[V], RowAcc<T, OP, RHO, V>& acc) {
+                                                const T (&hb)[V], const T (&rc)[3],
+                                                RowAcc<T, OP, RHO, V>& acc) {
   constexpr bool BIN = OP != OP_COPY;
   const int32_t* __restrict__ indices = a.indices;
   const int32_t* __restrict__ eids = a.eids;
@@ -287,7 +353,7 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
   const int lm = (MP == MP_GEN) ? a.lhs.mode : M_FULL;
   const int rm = !BIN ? M_NONE
                       : (MP == MP_FF ? M_FULL
-                                     : (MP == MP_FS ? M_SCALAR
+                                     : ((MP == MP_FS || IsAttn<MP>::value) ? M_SCALAR
                                                     : (MP == MP_FH ? M_HOIST : a.rhs.mode)));
   const bool l_eid = a.lhs.from_eid, r_eid = a.rhs.from_eid;
   // lane column base pointers (clamped in-bounds for masked columns)
@@ -318,7 +384,7 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
   T sa0 = T(0), sb0 = T(0);
   if (base + lane < pe) {
     if (lm == M_SCALAR) sa0 = scalar_at<T>(a.lhs, lrow(nb0, eb0, base));
-    if (rm == M_SCALAR) sb0 = scalar_at<T>(a.rhs, rrow(nb0, eb0, base));
+    if (rm == M_SCALAR) sb0 = rhs_scalar<T, MP>(a, rrow(nb0, eb0, base), rc);
   }
   int since_fold = 0;
   for (; base < pe; base += stride) {
@@ -333,7 +399,7 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
     T sa1 = T(0), sb1 = T(0);
     if (base + stride + lane < pe) {
       if (lm == M_SCALAR) sa1 = scalar_at<T>(a.lhs, lrow(nb1, eb1, base + stride));
-      if (rm == M_SCALAR) sb1 = scalar_at<T>(a.rhs, rrow(nb1, eb1, base + stride));
+      if (rm == M_SCALAR) sb1 = rhs_scalar<T, MP>(a, rrow(nb1, eb1, base + stride), rc);
     }
     const uint32_t ra_lane = lrow(nb0, eb0, base);
     const uint32_t rb_lane = rrow(nb0, eb0, base);
@@ -417,14 +483,14 @@ constexpr int kChunkE = 256;
 template <typename T, int OP, int RHO, int V, int MP, int U>
 __device__ __forceinline__ void spmm_accumulate_chunked(
     const SpmmArgs& a, int64_t pb, int64_t pe, int64_t first, int64_t stride, int lane, int slot,
-    int E, int col, bool valid, const T (&ha)[V], const T (&hb)[V], int32_t* sidx,
-    int32_t* seid, RowAcc<T, OP, RHO, V>& acc) {
+    int E, int col, bool valid, const T (&ha)[V], const T (&hb)[V], const T (&rc)[3],
+    int32_t* sidx, int32_t* seid, RowAcc<T, OP, RHO, V>& acc) {
   constexpr bool BIN = OP != OP_COPY;
   constexpr int B = kChunkE / 32;
   const int lm = (MP == MP_GEN) ? a.lhs.mode : M_FULL;
   const int rm = !BIN ? M_NONE
                       : (MP == MP_FF ? M_FULL
-                                     : (MP == MP_FS ? M_SCALAR
+                                     : ((MP == MP_FS || IsAttn<MP>::value) ? M_SCALAR
                                                     : (MP == MP_FH ? M_HOIST : a.rhs.mode)));
   const bool need_eid = a.need_eid;
   const int ccol = valid ? col : 0;
@@ -483,7 +549,7 @@ __device__ __forceinline__ void spmm_accumulate_chunked(
 #pragma unroll
           for (int k = 0; k < V; ++k) vb[u][k] = T(0);
         } else {
-          const T sb = (rm == M_SCALAR && ok[u]) ? scalar_at<T>(a.rhs, rb) : T(0);
+          const T sb = (rm == M_SCALAR && ok[u]) ? rhs_scalar<T, MP>(a, rb, rc) : T(0);
 #pragma unroll
           for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
         }
@@ -521,13 +587,13 @@ __device__ __forceinline__ void spmm_accumulate_chunked(
 template <typename T, int OP, int RHO, int V, int MP, int U>
 __device__ __forceinline__ void spmm_accumulate_slot(const SpmmArgs& a, int64_t pb, int64_t pe,
                                                      int col, bool valid, const T (&ha)[V],
-                                                     const T (&hb)[V],
+                                                     const T (&hb)[V], const T (&rc)[3],
                                                      RowAcc<T, OP, RHO, V>& acc) {
   constexpr bool BIN = OP != OP_COPY;
   const int lm = (MP == MP_GEN) ? a.lhs.mode : M_FULL;
   const int rm = !BIN ? M_NONE
                       : (MP == MP_FF ? M_FULL
-                                     : (MP == MP_FS ? M_SCALAR
+                                     : ((MP == MP_FS || IsAttn<MP>::value) ? M_SCALAR
                                                     : (MP == MP_FH ? M_HOIST : a.rhs.mode)));
   const bool need_eid = a.need_eid;
   const int ccol = valid ? col : 0;
@@ -565,7 +631,7 @@ __device__ __forceinline__ void spmm_accumulate_slot(const SpmmArgs& a, int64_t 
 #pragma unroll
         for (int k = 0; k < V; ++k) vb[u][k] = T(0);
       } else {
-        const T sb = (rm == M_SCALAR && ok[u]) ? scalar_at<T>(a.rhs, rb) : T(0);
+        const T sb = (rm == M_SCALAR && ok[u]) ? rhs_scalar<T, MP>(a, rb, rc) : T(0);
 #pragma unroll
         for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
       }
@@ -699,11 +765,16 @@ spmm_rows_kernel(const SpmmArgs a) {
     }
   }
 
+  T rc[3] = {T(0), T(0), T(0)};
+  if constexpr (IsAttn<MP>::value) {
+    if (deg > 0) attn_row_consts<T, MP>(a, row, rc);
+  }
+
   Acc acc;
   acc.init();
   if constexpr (NARROW) {
     if (light) {
-      spmm_accumulate_slot<T, OP, RHO, V, MP, U>(a, pb, pe, col, valid, ha, hb, acc);
+      spmm_accumulate_slot<T, OP, RHO, V, MP, U>(a, pb, pe, col, valid, ha, hb, rc, acc);
       if (row < 0) return;
       if (a.counts && tile == 0 && gl == 0) a.counts[row] = deg;
       write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
@@ -711,14 +782,14 @@ spmm_rows_kernel(const SpmmArgs a) {
     }
     spmm_accumulate_chunked<T, OP, RHO, V, MP, U>(
         a, pb, pe, heavy ? (int64_t)warp * kChunkE : 0,
-        heavy ? (int64_t)kChunkE * kWarpsPerCta : kChunkE, lane, slot, E, col, valid, ha, hb,
+        heavy ? (int64_t)kChunkE * kWarpsPerCta : kChunkE, lane, slot, E, col, valid, ha, hb, rc,
         s_chunk + warp * kChunkE, s_chunk + (kWarpsPerCta + warp) * kChunkE, acc);
   } else if (heavy) {
     spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, (int64_t)warp * 32, 32 * kWarpsPerCta, lane,
-                                          slot, E, col, valid, ha, hb, acc);
+                                          slot, E, col, valid, ha, hb, rc, acc);
   } else {
     spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, 0, 32, lane, slot, E, col, valid, ha, hb,
-                                          acc);
+                                          rc, acc);
   }
   acc.combine_slots(a.g_log2);
 
@@ -803,6 +874,11 @@ cudaError_t launch_spmm_rows_v(int V, int mp, const SpmmArgs& a, int64_t grid, c
   if (V == 2) return launch_spmm_rows_mp<T, OP, RHO, 2>(mp, a, grid, s);
   return launch_spmm_rows_mp<T, OP, RHO, 1>(mp, a, grid, s);
 }
+
+// fused GAT attention aggregation (u_mul_e + sum with recomputed weights):
+// spmm_op_attn.cu. backward = MP_AB on the reverse graph.
+cudaError_t launch_spmm_rows_attn(int dtype_is_f64, int V, bool backward, const SpmmArgs& a,
+                                  int64_t grid, cudaStream_t s);
 
 // dot messages under sum/mean (single column tile): spmm_op_dot.cu
 cudaError_t launch_spmm_rows_dot_sum(int dtype_is_f64, int V, int mp, const SpmmArgs& a,

@@ -602,3 +602,61 @@ def edge_softmax_uv_forward(g, el, er):
             _dtype_code(L), L.data_ptr(), _ld(L), R.data_ptr(), _ld(R), H, alpha.data_ptr(), H,
             ws.data_ptr(), ws_bytes, _stream(g.device)), "gmp_edge_softmax_uv_fwd")
     return alpha
+
+
+# ----------------------------------------------------------------------------
+# fused GAT attention (u_add_v -> edge_softmax -> u_mul_e + sum, layers.py:110-115)
+
+
+def edge_softmax_uv_stats(g, el, er):
+    """Per-destination statistics of the u_add_v scores el[src] + er[dst]:
+    (n, 2H) = [max_h | 1/sum_h exp(s - max_h)]; zero rows for destinations
+    without in-edges. The statistics pass of edge_softmax_uv_forward alone."""
+    _require_cuda(g)
+    L = _as_matrix("el", el, g.num_nodes, g.device)
+    R = _as_matrix("er", er, g.num_nodes, g.device)
+    if L.dtype != R.dtype or L.shape[1] != R.shape[1]:
+        raise ValueError("el and er need the same dtype and head count")
+    H = L.shape[1]
+    stat = torch.zeros((g.num_nodes, 2 * H), dtype=L.dtype, device=g.device)
+    if g.num_edges and H:
+        lib = _lib.load()
+        adj = g.to_csc()
+        sched = adj.schedule()
+        accounting.log_dispatch("gspmm", g.uid, "edge_softmax_stats(add(src,dst))", "softmax",
+                                "node_parallel", g.num_edges, H)
+        _lib.check(lib.gmp_edge_softmax_uv_stats(
+            ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), _dtype_code(L),
+            L.data_ptr(), _ld(L), R.data_ptr(), _ld(R), H, stat.data_ptr(),
+            stat.numel() * stat.element_size(), _stream(g.device)), "gmp_edge_softmax_uv_stats")
+    return stat
+
+
+def gat_aggregate(g, X, el, pack, backward=False):
+    """One head of the fused attention aggregation (gmp_gat_aggregate).
+    forward:  Z[v] = sum_{(u,e)->v} alpha_e X[u]   over g's in-adjacency
+    backward: Z[u] = sum_{(v,e): u->v} alpha_e X[v] over reverse(g)'s
+    with alpha_e = exp((el[u] + er[v]) - max[v]) * inv_sum[v] recomputed from
+    el (n, 1) and pack (n, 4) = [er, max, inv_sum, 0]."""
+    from .graph import reverse
+    _require_cuda(g)
+    X = _as_matrix("X", X, g.num_nodes, g.device)
+    d = X.shape[1]
+    Z = accounting.register(torch.empty((g.num_nodes, d), dtype=X.dtype, device=g.device))
+    if not Z.numel():
+        return Z
+    if el.dtype != X.dtype or pack.dtype != X.dtype:
+        raise ValueError("el / pack must have the feature dtype")
+    if not (pack.is_contiguous() and pack.shape == (g.num_nodes, 4)):
+        raise ValueError("pack must be a contiguous (n, 4) matrix")
+    walk = reverse(g) if backward else g
+    adj = walk.to_csc()
+    sched = adj.schedule()
+    accounting.log_dispatch("gspmm", walk.uid, "mul(src,edge_softmax(add(src,dst)))", "sum",
+                            "node_parallel", g.num_nodes, d)
+    lde = int(el.stride(0)) if el.shape[0] > 1 else 1
+    _lib.check(_lib.load().gmp_gat_aggregate(
+        ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), _dtype_code(X),
+        1 if backward else 0, X.data_ptr(), _ld(X), d, el.data_ptr(), lde, pack.data_ptr(),
+        Z.data_ptr(), _ld(Z), _ptr(_tuning_struct(None)), _stream(g.device)), "gmp_gat_aggregate")
+    return Z

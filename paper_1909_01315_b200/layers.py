@@ -12,11 +12,13 @@ they own no kernels. Semantics follow /root/reference/pkg/src/graphmp/layers.py:
 `aggregator="sum"` gives the copy_u+sum GCN named by BASELINE.json config 0.
 Dense projections are torch matmuls (cuBLAS; fp32 with TF32 off by default so
 parity tests compare against the reference's float64 numbers).
-The GAT head scores (u_add_v) and edge_softmax run as one fused kernel pair
-over (m, H) that never stores the scores; el / er come from X (W a) without the
-projection; the u_mul_e aggregation runs on the narrower of the input and
-the projected features (linearity: sum alpha (X W) = (sum alpha X) W), reading
-strided column views of the (n, H*D) projection, so no head copy is made.
+GAT (fused=True, default): el / er come from X (W a) without the projection;
+a statistics kernel computes each destination's softmax max / sum of the
+u_add_v scores, and the aggregation row kernels recompute every attention
+weight from node-keyed data, forward (destination rows) and backward
+(reverse-graph rows), so neither the (m, H) scores nor alpha are ever stored.
+The aggregation runs on the narrower of the input and the projected features
+(linearity: sum alpha (X W) = (sum alpha X) W).
 """
 
 from dataclasses import dataclass
@@ -118,8 +120,13 @@ def sage_layer(g, X, params, act="relu", order="auto", **kw):
     return _act(X @ Ws + aggregate(g, X, "mean", **kw) @ Wn, act)
 
 
-def gat_layer(g, X, params, num_heads=None, **kw):
-    """Heads concatenated column-wise; isolated destinations get zero rows."""
+def gat_layer(g, X, params, num_heads=None, fused=True, **kw):
+    """Heads concatenated column-wise; isolated destinations get zero rows.
+    fused=True: the attention weights are recomputed inside the aggregation
+    row kernels (gmp_gat_aggregate) and no (m, H) tensor exists in the forward
+    or the backward; fused=False: the fused u_add_v + edge_softmax kernel pair
+    writes alpha (m, H) and per-head u_mul_e g-SpMMs read it (the reference's
+    composition, layers.py:110-115)."""
     _check_rows(g, X)
     heads = params.heads if num_heads is None else params.heads[:num_heads]
     if not heads:
@@ -134,13 +141,19 @@ def gat_layer(g, X, params, num_heads=None, **kw):
     ar = torch.stack([_t(h.a_r, dev, dt)[:, 0] for h in heads])
     # el = proj . a_l = X (W a_l): only (d_in, H) extra weights, no projection needed
     Wv = Wcat.view(d_in, H, D)
-    el = X @ (Wv * al).sum(-1)                                            # (n, H)
-    er = X @ (Wv * ar).sum(-1)
+    el = (X @ (Wv * al).sum(-1)).contiguous()                             # (n, H)
+    er = (X @ (Wv * ar).sum(-1)).contiguous()
+    if fused:
+        if d_in < D:
+            # sum_u alpha_uv (X_u W) = (sum_u alpha_uv X_u) W: aggregate the narrower side
+            agg = autodiff.gat_attention(g, el, er, X, shared=True)       # (n, H*d_in)
+            outs = [agg[:, h * d_in:(h + 1) * d_in] @ Wv[:, h, :] for h in range(H)]
+        else:
+            return autodiff.gat_attention(g, el, er, X @ Wcat, shared=False)
+        return outs[0] if H == 1 else torch.cat(outs, dim=1)
     # u_add_v scores + edge_softmax fused: the (m, H) scores are never stored
-    alpha = autodiff.edge_softmax_uv(g, el.contiguous(), er.contiguous())  # (m, H)
+    alpha = autodiff.edge_softmax_uv(g, el, er)                           # (m, H)
     if d_in < D:
-        # sum_u alpha_uv (X_u W) = (sum_u alpha_uv X_u) W: aggregate the narrower
-        # side (same result up to rounding; the reference projects first)
         outs = [autodiff.gspmm(g, kernels.mul("src", "edge"), "sum", X=X,
                                W=alpha[:, h:h + 1], **kw) @ Wv[:, h, :] for h in range(H)]
     else:
@@ -230,9 +243,10 @@ class GATModel:
     last) - the Reddit GAT epoch of the paper is 3 layers x 16 hidden x 1 head
     (PAPER.md:965-966); the reference only defines the single gat_layer."""
 
-    def __init__(self, dims, heads=1, seed=0, device=None, dtype=torch.float32):
+    def __init__(self, dims, heads=1, seed=0, device=None, dtype=torch.float32, fused=True):
         rng = np.random.default_rng(seed)
         device = device or default_device()
+        self.fused = fused
         self.layers = []
         d_in = dims[0]
         for i, d_out in enumerate(dims[1:]):
@@ -251,7 +265,7 @@ class GATModel:
         h = x
         last = len(self.layers) - 1
         for i, p in enumerate(self.layers):
-            h = gat_layer(g, h, p, **kw)
+            h = gat_layer(g, h, p, fused=self.fused, **kw)
             if i < last:
                 h = torch.relu(h)
         return h

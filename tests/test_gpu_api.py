@@ -143,12 +143,14 @@ def test_gcn_training_losses_match_reference(order):
     assert np.allclose(l32, want, rtol=1e-5, atol=1e-6)
 
 
-def test_gat_layer_matches_reference():
+@pytest.mark.parametrize("fused", [True, False])
+def test_gat_layer_matches_reference(fused):
     gd = golden()
     src, dst, n = golden_graph("gcn")
     g = G.from_arrays(src.astype(np.int64), dst.astype(np.int64), n, device=DEV)
     params = layers.init_gat(np.random.default_rng(1), 12, 4, 3)
-    h = layers.gat_layer(g, torch.as_tensor(gd["gcn/x"].astype(np.float64), device=DEV), params)
+    h = layers.gat_layer(g, torch.as_tensor(gd["gcn/x"].astype(np.float64), device=DEV), params,
+                         fused=fused)
     assert rel_err(to_np(h), gd["gat/out"]) < 1e-10
 
 

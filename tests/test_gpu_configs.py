@@ -37,8 +37,9 @@ def test_c1_cora_gcn_loss_curve(gold, dtype, rtol):
     assert np.allclose(losses, gold["c1/losses"], rtol=rtol, atol=1e-7), (losses, gold["c1/losses"])
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-def test_c2_pubmed_gat_layer_fwd_bwd(gold, dtype):
+def test_c2_pubmed_gat_layer_fwd_bwd(gold, dtype, fused):
     src, dst, n, x, u = c2_inputs()
     g = G.from_arrays(src, dst, num_nodes=n, device=DEV)
     params = layers.init_gat(np.random.default_rng(7), 500, 8, 8)
@@ -48,7 +49,7 @@ def test_c2_pubmed_gat_layer_fwd_bwd(gold, dtype):
                                 for a in (hp.W, hp.a_l, hp.a_r))
         leaves.append((hp.W, hp.a_l, hp.a_r))
     xt = torch.as_tensor(x, device=DEV).to(dtype)
-    h = layers.gat_layer(g, xt, params)
+    h = layers.gat_layer(g, xt, params, fused=fused)
     (h * torch.as_tensor(u, device=DEV).to(dtype)).sum().backward()
     tol = 1e-10 if dtype == torch.float64 else 2e-5
     assert rel_err(to_np(h)[SAMPLE_ROWS], gold["c2/h_rows"]) < tol
