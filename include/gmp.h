@@ -189,17 +189,20 @@ int gmp_edge_softmax_uv_stats(const gmp_adj* in_adj, const gmp_sched* sched, int
  * One head of the reference's GAT aggregation (layers.py:110-115: u_add_v ->
  * edge_softmax -> u_mul_e + sum) with the attention weights never stored:
  *   alpha_e = exp((el[src e] + er[dst e]) - max[dst e]) * inv_sum[dst e]
- * pack: (n, 4) rows [er, max, inv_sum, 0] (max / inv_sum from
- * gmp_edge_softmax_uv_stats), el: (n) with stride lde.
+ * pack: (n, 4) rows [er, max, inv_sum, w] (max / inv_sum from
+ * gmp_edge_softmax_uv_stats; w is read by the backward only), el: (n) with
+ * stride lde.
  * backward == 0: adj = in-adjacency, Z[v] = sum_{(u,e)->v} alpha_e X[u]
  * backward == 1: adj = the reverse graph's in-adjacency (= forward CSR),
  *                Z[u] = sum_{(v,e): u->v} alpha_e X[v]  (X = upstream grad rows,
- *                the transposed aggregation of Theorem 1).
+ *                the transposed aggregation of Theorem 1), and, when t_out is
+ *                not NULL, t_out[u] = sum_{(v,e): u->v} alpha_e w[v] (fp64) -
+ *                the softmax-backward term of d el.
  * X: (n, d) with ldx, Z: (n, d) with ldz. */
 int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int backward,
                       const void* X, int64_t ldx, int32_t d, const void* el, int64_t lde,
-                      const void* pack, void* Z, int64_t ldz, const gmp_tuning* tuning,
-                      void* stream);
+                      const void* pack, void* Z, int64_t ldz, double* t_out,
+                      const gmp_tuning* tuning, void* stream);
 
 /* ---- extrema gradient routing ----------------------------------------------
  * Replaces kernels.route_extrema_grad (kernels.py:843-857): dM[arg[v,k], k] =

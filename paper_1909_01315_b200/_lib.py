@@ -89,7 +89,7 @@ def _declare(lib):
     lib.gmp_edge_softmax_uv_stats.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, vp, i64, vp, i64,
                                               i32, vp, ctypes.c_size_t, vp]
     lib.gmp_gat_aggregate.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, c_int, vp, i64, i32, vp,
-                                      i64, vp, vp, i64, _P(GmpTuning), vp]
+                                      i64, vp, vp, i64, vp, _P(GmpTuning), vp]
     lib.gmp_last_error.restype = ctypes.c_char_p
     lib.gmp_strerror.argtypes = [c_int]
     lib.gmp_strerror.restype = ctypes.c_char_p

@@ -306,7 +306,8 @@ class _GATAttention(torch.autograd.Function):
                  S_v = sum_{e'->v} alpha_e' g_e' = dZ_h[v] . Z_h[v]
                = X_h[u] . dX_h[u] - sum_{u->v} alpha_e S_v
       d er[v]  = S_v (1 - sum_{e->v} alpha_e) = 0   (softmax is shift-invariant)
-    The S_v column rides along the dX aggregation as an extra column."""
+    S_v rides in the 4th column of the per-node pack the kernel gathers
+    anyway; the reverse-graph kernel returns t[u] = sum_{u->v} alpha_e S_v."""
 
     @staticmethod
     def forward(ctx, g, el, er, X, shared):
@@ -333,20 +334,17 @@ class _GATAttention(torch.autograd.Function):
         g, shared, d = ctx.g, ctx.shared, ctx.d
         H = el.shape[1]
         dout = dout.to(X.dtype)
-        dp = (d + 1 + 3) // 4 * 4
         acc = torch.float64
         dX_parts, del_cols = [], []
         for h in range(H):
             dZh = dout[:, h * d:(h + 1) * d]
             Zh = out[:, h * d:(h + 1) * d]
-            S = (dZh.to(acc) * Zh.to(acc)).sum(1)
-            G2 = torch.zeros((g.num_nodes, dp), dtype=X.dtype, device=X.device)
-            G2[:, :d] = dZh
-            G2[:, d] = S.to(X.dtype)
-            R = kernels.gat_aggregate(g, G2, el[:, h:h + 1], pack[h], backward=True)
-            dXh = R[:, :d]
+            # S_v rides in the pack's 4th column; t[u] = sum_{u->v} alpha_e S_v
+            pk = pack[h].clone()
+            pk[:, 3] = (dZh.to(acc) * Zh.to(acc)).sum(1).to(X.dtype)
+            dXh, t = kernels.gat_aggregate(g, dZh, el[:, h:h + 1], pk, backward=True)
             Xh = X if shared else X[:, h * d:(h + 1) * d]
-            del_cols.append(((Xh.to(acc) * dXh.to(acc)).sum(1) - R[:, d].to(acc)).to(X.dtype))
+            del_cols.append(((Xh.to(acc) * dXh.to(acc)).sum(1) - t).to(X.dtype))
             dX_parts.append(dXh)
         if shared:
             dX = dX_parts[0]

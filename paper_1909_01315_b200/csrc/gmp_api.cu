@@ -550,8 +550,8 @@ int gmp_edge_softmax_uv_stats(const gmp_adj* in_adj, const gmp_sched* sched, int
 
 int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int backward,
                       const void* X, int64_t ldx, int32_t d, const void* el, int64_t lde,
-                      const void* pack, void* Z, int64_t ldz, const gmp_tuning* tuning,
-                      void* stream) {
+                      const void* pack, void* Z, int64_t ldz, double* t_out,
+                      const gmp_tuning* tuning, void* stream) {
   if (!adj) return fail(GMP_EINVAL, "null adjacency");
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
   if (adj->m < 0 || adj->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
@@ -591,6 +591,7 @@ int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int
   a.need_eid = 0;
   a.Z = Z; a.ldz = ldz;
   a.attn_el = el; a.attn_lde = (uint32_t)lde; a.attn_pack = pack;
+  a.attn_t = backward ? t_out : nullptr;
   const int64_t grid = bpt_rows * ntiles;
   if (grid >= (1ll << 31)) return fail(GMP_EUNSUPPORTED, "grid too large");
   cudaError_t e = launch_spmm_rows_attn(F == 8, V, backward != 0, a, grid, (cudaStream_t)stream);

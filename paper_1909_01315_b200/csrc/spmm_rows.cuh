@@ -96,17 +96,19 @@ struct SpmmArgs {
   // fused attention (MP_AF / MP_AB only)
   const void* attn_el;    // (n) el column, stride attn_lde
   uint32_t attn_lde;
-  const void* attn_pack;  // (n, 4) rows [er, max, inv_sum, 0]
+  const void* attn_pack;  // (n, 4) rows [er, max, inv_sum, w]
+  double* attn_t;         // MP_AB: t[u] = sum_{u->v} alpha_e w[v] (nullable)
 };
 
 template <typename T>
-__device__ __forceinline__ void load_pack3(const T* p, T& a, T& b, T& c) {
+__device__ __forceinline__ void load_pack4(const T* p, T& a, T& b, T& c, T& d) {
   if constexpr (sizeof(T) == 4) {
     const float4 v = __ldg(reinterpret_cast<const float4*>(p));
-    a = v.x; b = v.y; c = v.z;
+    a = v.x; b = v.y; c = v.z; d = v.w;
   } else {
     const double2 v0 = __ldg(reinterpret_cast<const double2*>(p));
-    a = v0.x; b = v0.y; c = __ldg(p + 2);
+    const double2 v1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    a = v0.x; b = v0.y; c = v1.x; d = v1.y;
   }
 }
 
@@ -117,7 +119,8 @@ __device__ __forceinline__ void attn_row_consts(const SpmmArgs& a, int64_t row, 
   rc[0] = rc[1] = rc[2] = T(0);
   if (row < 0) return;
   if constexpr (MP == MP_AF) {
-    load_pack3<T>(static_cast<const T*>(a.attn_pack) + row * 4, rc[0], rc[1], rc[2]);
+    T w;
+    load_pack4<T>(static_cast<const T*>(a.attn_pack) + row * 4, rc[0], rc[1], rc[2], w);
   } else if constexpr (MP == MP_AB) {
     rc[0] = __ldg(static_cast<const T*>(a.attn_el) + (uint64_t)row * a.attn_lde);
   }
@@ -127,25 +130,36 @@ __device__ __forceinline__ float attn_exp(float x) { return expf(x); }
 __device__ __forceinline__ double attn_exp(double x) { return exp(x); }
 
 // attention weight of the edge to/from neighbour nb; same fp operation
-// order as the fused softmax (softmax.cuh: s = el + er; exp(s - max) * inv)
+// order as the fused softmax (softmax.cuh: s = el + er; exp(s - max) * inv).
+// MP_AB also returns the neighbour's pack w (the backward's per-destination
+// sum S_v) in w.
 template <typename T, int MP>
-__device__ __forceinline__ T attn_alpha(const SpmmArgs& a, uint32_t nb, const T (&rc)[3]) {
+__device__ __forceinline__ T attn_alpha(const SpmmArgs& a, uint32_t nb, const T (&rc)[3], T& w) {
   if constexpr (MP == MP_AF) {
+    w = T(0);
     const T x = __ldg(static_cast<const T*>(a.attn_el) + (uint64_t)nb * a.attn_lde) + rc[0];
     return attn_exp(T(x - rc[1])) * rc[2];
   } else {
     T er, mx, inv;
-    load_pack3<T>(static_cast<const T*>(a.attn_pack) + (uint64_t)nb * 4, er, mx, inv);
+    load_pack4<T>(static_cast<const T*>(a.attn_pack) + (uint64_t)nb * 4, er, mx, inv, w);
     const T x = rc[0] + er;
     return attn_exp(T(x - mx)) * inv;
   }
 }
 
-// per-edge scalar operand: a stored scalar, or the recomputed attention weight
+// per-edge scalar operand: a stored scalar, or the recomputed attention
+// weight (MP_AB adds alpha * w of the edge into tsum)
 template <typename T, int MP>
-__device__ __forceinline__ T rhs_scalar(const SpmmArgs& a, uint32_t row, const T (&rc)[3]) {
-  if constexpr (IsAttn<MP>::value) return attn_alpha<T, MP>(a, row, rc);
-  else return __ldg(static_cast<const T*>(a.rhs.data) + (uint64_t)row * a.rhs.ld);
+__device__ __forceinline__ T rhs_scalar(const SpmmArgs& a, uint32_t row, const T (&rc)[3],
+                                        double& tsum) {
+  if constexpr (IsAttn<MP>::value) {
+    T w;
+    const T al = attn_alpha<T, MP>(a, row, rc, w);
+    if constexpr (MP == MP_AB) tsum += (double)al * (double)w;
+    return al;
+  } else {
+    return __ldg(static_cast<const T*>(a.rhs.data) + (uint64_t)row * a.rhs.ld);
+  }
 }
 
 // ---- accumulation policies ---------------------------------------------------
@@ -190,8 +204,10 @@ struct RowAcc {
   float s[V], c[V];
   ExtT cur[V];
   int32_t arg[V];
+  double tsum;  // MP_AB only: sum of alpha_e * w over the edges this lane prefetched
 
   __device__ __forceinline__ void init() {
+    tsum = 0.0;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       acc[k] = 0.0;
@@ -384,7 +400,7 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
   T sa0 = T(0), sb0 = T(0);
   if (base + lane < pe) {
     if (lm == M_SCALAR) sa0 = scalar_at<T>(a.lhs, lrow(nb0, eb0, base));
-    if (rm == M_SCALAR) sb0 = rhs_scalar<T, MP>(a, rrow(nb0, eb0, base), rc);
+    if (rm == M_SCALAR) sb0 = rhs_scalar<T, MP>(a, rrow(nb0, eb0, base), rc, acc.tsum);
   }
   int since_fold = 0;
   for (; base < pe; base += stride) {
@@ -399,7 +415,7 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
     T sa1 = T(0), sb1 = T(0);
     if (base + stride + lane < pe) {
       if (lm == M_SCALAR) sa1 = scalar_at<T>(a.lhs, lrow(nb1, eb1, base + stride));
-      if (rm == M_SCALAR) sb1 = rhs_scalar<T, MP>(a, rrow(nb1, eb1, base + stride), rc);
+      if (rm == M_SCALAR) sb1 = rhs_scalar<T, MP>(a, rrow(nb1, eb1, base + stride), rc, acc.tsum);
     }
     const uint32_t ra_lane = lrow(nb0, eb0, base);
     const uint32_t rb_lane = rrow(nb0, eb0, base);
@@ -515,7 +531,15 @@ __device__ __forceinline__ void spmm_accumulate_chunked(
 #pragma unroll
     for (int i = 0; i < B; ++i) {
       sidx[i * 32 + lane] = pn[i];
-      seid[i * 32 + lane] = pe_[i];
+      if constexpr (IsAttn<MP>::value && sizeof(T) == 4) {
+        // the attention weight of each staged edge, computed once per edge
+        // (not once per feature lane) and kept in the edge-id slot
+        float al = 0.f;
+        if (cb + i * 32 + lane < pe) al = rhs_scalar<T, MP>(a, (uint32_t)pn[i], rc, acc.tsum);
+        seid[i * 32 + lane] = __float_as_int(al);
+      } else {
+        seid[i * 32 + lane] = pe_[i];
+      }
     }
     __syncwarp();
     fetch(cb + stride);
@@ -549,7 +573,13 @@ __device__ __forceinline__ void spmm_accumulate_chunked(
 #pragma unroll
           for (int k = 0; k < V; ++k) vb[u][k] = T(0);
         } else {
-          const T sb = (rm == M_SCALAR && ok[u]) ? rhs_scalar<T, MP>(a, rb, rc) : T(0);
+          T sb;
+          if constexpr (IsAttn<MP>::value && sizeof(T) == 4) {
+            sb = __int_as_float(eb);  // staged attention weight
+          } else {
+            double dummy = 0.0;
+            sb = (rm == M_SCALAR && ok[u]) ? rhs_scalar<T, MP>(a, rb, rc, dummy) : T(0);
+          }
 #pragma unroll
           for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
         }
@@ -603,6 +633,8 @@ __device__ __forceinline__ void spmm_accumulate_slot(const SpmmArgs& a, int64_t 
   const uint32_t rld = a.rhs.ld * (uint32_t)sizeof(T);
   const int cnt = (int)(pe - pb);
   const int max_cnt = __reduce_max_sync(kFull, (unsigned)cnt);
+  // every lane of a slot computes the same edge's weight; one lane sums alpha*w
+  const bool t_owner = ((threadIdx.x & 31) & ((1 << a.g_log2) - 1)) == 0;
   for (int t = 0; t < max_cnt; t += U) {
     T va[U][V], vb[U][V];
     int32_t ee[U];
@@ -631,7 +663,10 @@ __device__ __forceinline__ void spmm_accumulate_slot(const SpmmArgs& a, int64_t 
 #pragma unroll
         for (int k = 0; k < V; ++k) vb[u][k] = T(0);
       } else {
-        const T sb = (rm == M_SCALAR && ok[u]) ? rhs_scalar<T, MP>(a, rb, rc) : T(0);
+        double tdummy = 0.0;
+        const T sb = (rm == M_SCALAR && ok[u])
+                         ? rhs_scalar<T, MP>(a, rb, rc, t_owner ? acc.tsum : tdummy)
+                         : T(0);
 #pragma unroll
         for (int k = 0; k < V; ++k) vb[u][k] = (rm == M_SCALAR) ? sb : hb[k];
       }
@@ -776,6 +811,9 @@ spmm_rows_kernel(const SpmmArgs a) {
     if (light) {
       spmm_accumulate_slot<T, OP, RHO, V, MP, U>(a, pb, pe, col, valid, ha, hb, rc, acc);
       if (row < 0) return;
+      if constexpr (MP == MP_AB) {
+        if (a.attn_t && tile == 0 && gl == 0) a.attn_t[row] = acc.tsum;
+      }
       if (a.counts && tile == 0 && gl == 0) a.counts[row] = deg;
       write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
       return;
@@ -792,13 +830,23 @@ spmm_rows_kernel(const SpmmArgs a) {
                                           rc, acc);
   }
   acc.combine_slots(a.g_log2);
+  if constexpr (MP == MP_AB) {  // every lane summed alpha*w of its own edges
+    for (int off = 16; off > 0; off >>= 1) acc.tsum += __shfl_xor_sync(kFull, acc.tsum, off);
+  }
 
   if (a.counts && tile == 0 && ((heavy && threadIdx.x == 0) || (!heavy && lane == 0)))
     a.counts[row] = deg;
 
   if (!heavy) {
     if (slot == 0) write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
+    if constexpr (MP == MP_AB) {
+      if (a.attn_t && tile == 0 && lane == 0) a.attn_t[row] = acc.tsum;
+    }
     return;
+  }
+  __shared__ double s_t[IsAttn<MP>::value ? kWarpsPerCta : 1];
+  if constexpr (MP == MP_AB) {
+    if (lane == 0) s_t[warp] = acc.tsum;
   }
   // CTA mode: merge the warp partials in warp order through shared memory.
   if (slot == 0) {
@@ -829,6 +877,13 @@ spmm_rows_kernel(const SpmmArgs a) {
       }
     }
     write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
+    if constexpr (MP == MP_AB) {
+      if (a.attn_t && tile == 0 && lane == 0) {
+        double t = s_t[0];
+        for (int w = 1; w < kWarpsPerCta; ++w) t += s_t[w];
+        a.attn_t[row] = t;
+      }
+    }
   }
 }
 

@@ -635,16 +635,18 @@ def edge_softmax_uv_stats(g, el, er):
 def gat_aggregate(g, X, el, pack, backward=False):
     """One head of the fused attention aggregation (gmp_gat_aggregate).
     forward:  Z[v] = sum_{(u,e)->v} alpha_e X[u]   over g's in-adjacency
-    backward: Z[u] = sum_{(v,e): u->v} alpha_e X[v] over reverse(g)'s
+    backward: Z[u] = sum_{(v,e): u->v} alpha_e X[v] over reverse(g)'s, and
+              t[u] = sum_{(v,e): u->v} alpha_e w[v] (fp64); returns (Z, t)
     with alpha_e = exp((el[u] + er[v]) - max[v]) * inv_sum[v] recomputed from
-    el (n, 1) and pack (n, 4) = [er, max, inv_sum, 0]."""
+    el (n, 1) and pack (n, 4) = [er, max, inv_sum, w]."""
     from .graph import reverse
     _require_cuda(g)
     X = _as_matrix("X", X, g.num_nodes, g.device)
     d = X.shape[1]
     Z = accounting.register(torch.empty((g.num_nodes, d), dtype=X.dtype, device=g.device))
+    t = torch.zeros(g.num_nodes if backward else 0, dtype=torch.float64, device=g.device)
     if not Z.numel():
-        return Z
+        return (Z, t) if backward else Z
     if el.dtype != X.dtype or pack.dtype != X.dtype:
         raise ValueError("el / pack must have the feature dtype")
     if not (pack.is_contiguous() and pack.shape == (g.num_nodes, 4)):
@@ -658,5 +660,6 @@ def gat_aggregate(g, X, el, pack, backward=False):
     _lib.check(_lib.load().gmp_gat_aggregate(
         ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), _dtype_code(X),
         1 if backward else 0, X.data_ptr(), _ld(X), d, el.data_ptr(), lde, pack.data_ptr(),
-        Z.data_ptr(), _ld(Z), _ptr(_tuning_struct(None)), _stream(g.device)), "gmp_gat_aggregate")
-    return Z
+        Z.data_ptr(), _ld(Z), t.data_ptr() if backward else None, _ptr(_tuning_struct(None)),
+        _stream(g.device)), "gmp_gat_aggregate")
+    return (Z, t) if backward else Z

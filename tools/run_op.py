@@ -30,6 +30,8 @@ def main():
     p.add_argument("--l2mb", type=int, default=0)
     p.add_argument("--rmat", type=int, default=0, help="RMAT edge count (nodes = --nodes)")
     p.add_argument("--l2fetch", type=int, default=0, help="cudaLimitMaxL2FetchGranularity bytes")
+    p.add_argument("--profile", action="store_true",
+                   help="cudaProfilerStart/Stop around the timed reps (ncu --profile-from-start off)")
     a = p.parse_args()
     dev = torch.device("cuda")
     torch.zeros(1, device=dev)
@@ -92,6 +94,8 @@ def main():
         torch.cuda.synchronize()
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         ts = []
+        if a.profile:
+            torch.cuda.profiler.start()
         for _ in range(a.reps):
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -100,6 +104,8 @@ def main():
             e1.record()
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
+        if a.profile:
+            torch.cuda.profiler.stop()
     if a.time:
         print("%s feat=%d tile=%d l2mb=%d: median %.3f ms (all %s)" % (
             a.op, F, a.tile_cols, a.l2mb, float(np.median(ts)), [round(t, 3) for t in ts]))
