@@ -228,6 +228,18 @@ int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* ar
 int gmp_gather_rows(int64_t n, int32_t dim, int dtype, const int32_t* idx, const void* src,
                     int64_t lds, void* dst, int64_t ldd, void* stream);
 
+/* ---- column-tile packing ----------------------------------------------------
+ * packed (ceil(d/tile), n, tile): packed[t][r][c] = src[r][t*tile + c], zero
+ * past column d. A g-SpMM over a wide src operand then runs one launch per
+ * column tile on packed[t] (ld = tile): each per-edge gather is an aligned
+ * run of whole sectors read with 128-bit loads, whatever src's ld (the
+ * reference's feature_parallel column split, kernels.py:485-513, laid out
+ * for L2 residency). gmp_unpack_tiles writes dst[r][c] for c < d back. */
+int gmp_pack_tiles(int64_t n, int32_t d, int dtype, int32_t tile, const void* src, int64_t lds,
+                   void* packed, void* stream);
+int gmp_unpack_tiles(int64_t n, int32_t d, int dtype, int32_t tile, const void* packed, void* dst,
+                     int64_t ldd, void* stream);
+
 /* ---- neighbour sampling ------------------------------------------------------
  * Replaces graph.neighbor_sample's per-seed draw (graph.py:231-266): for seed
  * i (node seeds[i], in-edges indptr[seeds[i]] .. indptr[seeds[i]+1] of the

@@ -26,6 +26,8 @@ cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const
 size_t schedule_workspace_bytes(int64_t n);
 cudaError_t launch_gather_rows(int, int64_t, int32_t, const int32_t*, const void*, int64_t, void*,
                                int64_t, cudaStream_t);
+cudaError_t launch_pack_tiles(int, bool, int64_t, int32_t, int32_t, const void*, int64_t, void*,
+                              int64_t, cudaStream_t);
 cudaError_t launch_neighbor_sample(const int64_t*, const int64_t*, int64_t, const int64_t*, uint64_t,
                                    int64_t*, int64_t*, cudaStream_t);
 cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t light,
@@ -597,6 +599,30 @@ int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int
   cudaError_t e = launch_spmm_rows_attn(F == 8, V, backward != 0, a, grid, (cudaStream_t)stream);
   g_launches++;
   return cuda_status(e, "gmp_gat_aggregate");
+}
+
+int gmp_pack_tiles(int64_t n, int32_t d, int dtype, int32_t tile, const void* src, int64_t lds,
+                   void* packed, void* stream) {
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (n < 0 || d < 0 || tile < 1 || lds < d) return fail(GMP_EINVAL, "bad sizes");
+  if (n == 0 || d == 0) return GMP_OK;
+  if (!src || !packed) return fail(GMP_EINVAL, "null arrays");
+  cudaError_t e = launch_pack_tiles(dtype == GMP_F64, false, n, d, tile, src, lds, packed, 0,
+                                    (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_pack_tiles");
+}
+
+int gmp_unpack_tiles(int64_t n, int32_t d, int dtype, int32_t tile, const void* packed, void* dst,
+                     int64_t ldd, void* stream) {
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (n < 0 || d < 0 || tile < 1 || ldd < d) return fail(GMP_EINVAL, "bad sizes");
+  if (n == 0 || d == 0) return GMP_OK;
+  if (!dst || !packed) return fail(GMP_EINVAL, "null arrays");
+  cudaError_t e = launch_pack_tiles(dtype == GMP_F64, true, n, d, tile, packed, 0, dst, ldd,
+                                    (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_unpack_tiles");
 }
 
 int gmp_neighbor_sample(const int64_t* indptr, int64_t n_rows, const int64_t* seeds,

@@ -55,7 +55,22 @@ static void sddmm_op(int op, int V, const SddmmArgs& a, int64_t grid, cudaStream
   }
 }
 
+template <typename T>
+static void sddmm_dot_lane(int V, const SddmmArgs& a, cudaStream_t s) {
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((a.m + 255) / 256, 148 * 8));
+  if constexpr (sizeof(T) == 4) {
+    if (V == 4) { sddmm_dot_lane_kernel<T, 4><<<(unsigned)grid, 256, 0, s>>>(a); return; }
+  }
+  if (V == 2) { sddmm_dot_lane_kernel<T, 2><<<(unsigned)grid, 256, 0, s>>>(a); return; }
+  sddmm_dot_lane_kernel<T, 1><<<(unsigned)grid, 256, 0, s>>>(a);
+}
+
 cudaError_t launch_sddmm(int f64, int op, int V, const SddmmArgs& a, int64_t grid, cudaStream_t s) {
+  if (op == OP_DOT && a.dim * (f64 ? 8 : 4) <= 128) {  // one operand row per 128 B line
+    if (f64) sddmm_dot_lane<double>(V, a, s);
+    else sddmm_dot_lane<float>(V, a, s);
+    return cudaGetLastError();
+  }
   if (f64) sddmm_op<double>(op, V, a, grid, s);
   else sddmm_op<float>(op, V, a, grid, s);
   return cudaGetLastError();
@@ -183,6 +198,55 @@ cudaError_t launch_gather_rows(int f64, int64_t n, int32_t dim, const int32_t* i
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
   if (f64) gather_rows_kernel<double><<<grid, 256, 0, s>>>(n, dim, idx, (const double*)src, lds, (double*)dst, ldd);
   else gather_rows_kernel<float><<<grid, 256, 0, s>>>(n, dim, idx, (const float*)src, lds, (float*)dst, ldd);
+  return cudaGetLastError();
+}
+
+// ---- column-tile packing ------------------------------------------------------
+// packed[t][r][c] = src[r][t*tw + c] (0 past column d): every column tile of a
+// row becomes one aligned tw-element run, so the row kernel's per-edge gather
+// of a tile is whole 32 B sectors with 128-bit loads whatever the caller's ld.
+
+template <typename T>
+__global__ void pack_tiles_kernel(int64_t n, int32_t d, int32_t tw, int32_t ntiles,
+                                  const T* __restrict__ src, int64_t lds, T* __restrict__ dst) {
+  const int64_t total = (int64_t)ntiles * n * tw;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % tw);
+    const int64_t tr = i / tw;
+    const int64_t r = tr % n;
+    const int t = (int)(tr / n);
+    const int col = t * tw + c;
+    dst[i] = col < d ? src[r * lds + col] : T(0);
+  }
+}
+
+template <typename T>
+__global__ void unpack_tiles_kernel(int64_t n, int32_t d, int32_t tw, const T* __restrict__ src,
+                                    T* __restrict__ dst, int64_t ldd) {
+  const int64_t total = n * (int64_t)d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d;
+    const int col = (int)(i - r * d);
+    const int t = col / tw;
+    dst[r * ldd + col] = src[((int64_t)t * n + r) * tw + (col - t * tw)];
+  }
+}
+
+cudaError_t launch_pack_tiles(int f64, bool unpack, int64_t n, int32_t d, int32_t tw,
+                              const void* src, int64_t lds, void* dst, int64_t ldd,
+                              cudaStream_t s) {
+  const int32_t ntiles = (d + tw - 1) / tw;
+  const int64_t total = unpack ? n * (int64_t)d : (int64_t)ntiles * n * tw;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 32));
+  if (f64) {
+    if (unpack) unpack_tiles_kernel<double><<<grid, 256, 0, s>>>(n, d, tw, (const double*)src, (double*)dst, ldd);
+    else pack_tiles_kernel<double><<<grid, 256, 0, s>>>(n, d, tw, ntiles, (const double*)src, lds, (double*)dst);
+  } else {
+    if (unpack) unpack_tiles_kernel<float><<<grid, 256, 0, s>>>(n, d, tw, (const float*)src, (float*)dst, ldd);
+    else pack_tiles_kernel<float><<<grid, 256, 0, s>>>(n, d, tw, ntiles, (const float*)src, lds, (float*)dst);
+  }
   return cudaGetLastError();
 }
 

@@ -106,6 +106,52 @@ __global__ void __launch_bounds__(256) sddmm_kernel(const SddmmArgs a) {
   }
 }
 
+// Narrow dot messages (dim <= 32 floats / 16 doubles): one edge per lane.
+// Consecutive lanes own consecutive edges, so the (src, dst) loads and the
+// M stores are coalesced; each lane reads its two operand rows with vector
+// loads (one 128 B line each at most) and forms the exact dot product as a
+// compensated fp32 pair (TwoProduct + TwoSum on packed FFMA2 / FADD2),
+// rounded once through fp64 - no shuffles and no per-element conversions.
+template <typename T, int V>
+__global__ void __launch_bounds__(256) sddmm_dot_lane_kernel(const SddmmArgs a) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.m; e += stride) {
+    const int32_t u = __ldg(a.src + e), v = __ldg(a.dst + e);
+    const T* pa = static_cast<const T*>(a.lhs.data) + operand_row(a.lhs, u, v, e) * a.lhs.ld;
+    const T* pb = static_cast<const T*>(a.rhs.data) + operand_row(a.rhs, u, v, e) * a.rhs.ld;
+    double r;
+    if constexpr (sizeof(T) == 4 && V >= 2) {
+      float2 S = f2(0.f, 0.f), C = f2(0.f, 0.f);
+#pragma unroll 4
+      for (int c = 0; c < a.dim; c += V) {
+        T xa[V], xb[V];
+        load_vec<T, V>(pa + c, xa);
+        load_vec<T, V>(pb + c, xb);
+#pragma unroll
+        for (int k = 0; k < V; k += 2) {
+          const float2 x = f2(xa[k], xa[k + 1]), y = f2(xb[k], xb[k + 1]);
+          const float2 pr = __fmul2_rn(x, y);
+          two_sum2(S, C, pr);
+          C = __fadd2_rn(C, __ffma2_rn(x, y, f2(-pr.x, -pr.y)));
+        }
+      }
+      r = ((double)S.x + (double)S.y) + ((double)C.x + (double)C.y);
+    } else {
+      ColSum<T> cs;
+#pragma unroll 4
+      for (int c = 0; c < a.dim; c += V) {
+        T xa[V], xb[V];
+        load_vec<T, V>(pa + c, xa);
+        load_vec<T, V>(pb + c, xb);
+#pragma unroll
+        for (int k = 0; k < V; ++k) cs.add_prod(xa[k], xb[k]);
+      }
+      r = cs.value();
+    }
+    static_cast<T*>(a.M)[e * a.ldm] = (T)r;
+  }
+}
+
 cudaError_t launch_sddmm(int dtype_is_f64, int op, int V, const SddmmArgs& a, int64_t grid,
                          cudaStream_t s);
 

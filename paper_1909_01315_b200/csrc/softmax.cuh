@@ -266,17 +266,39 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
 // ds[e]    = alpha[e] * (g[e] - sum[dst e])            (bwd)
 // Edge-id order: s / g / alpha / ds stream coalesced; the per-destination
 // statistics (T pairs, (n, H)) are L2-resident gathers. Each thread keeps
-// kApplyU independent vectors in flight.
+// kApplyU independent vectors in flight, and the destination ids of its next
+// group are loaded while the current group computes, so the dependent
+// statistics gather is not serialised behind a DRAM miss on dst[e].
 constexpr int kApplyU = 4;
 
 template <typename T, int V, bool BWD, bool UV>
 __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxArgs a) {
   const int per_edge = a.H / V;  // vectors per edge row
+  const int pe_log2 = (per_edge & (per_edge - 1)) == 0 ? __ffs(per_edge) - 1 : -1;
   const int64_t total = a.m * (int64_t)per_edge;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t step = nthreads * kApplyU;
   const T* st = static_cast<const T*>(a.stat);
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < total;
-       i0 += nthreads * kApplyU) {
+  auto edge_of = [&](int64_t i) -> int64_t {
+    return pe_log2 >= 0 ? (i >> pe_log2) : i / per_edge;
+  };
+  int32_t vn[kApplyU], un[kApplyU];
+  auto fetch_ids = [&](int64_t ib) {
+#pragma unroll
+    for (int u = 0; u < kApplyU; ++u) {
+      const int64_t i = ib + u * nthreads;
+      const int64_t e = i < total ? edge_of(i) : 0;
+      vn[u] = i < total ? __ldg(a.dst + e) : 0;
+      if constexpr (UV) un[u] = i < total ? __ldg(a.src + e) : 0;
+    }
+  };
+  int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  fetch_ids(i0);
+  for (; i0 < total; i0 += step) {
+    int32_t vc[kApplyU], uc[kApplyU];
+#pragma unroll
+    for (int u = 0; u < kApplyU; ++u) { vc[u] = vn[u]; uc[u] = UV ? un[u] : 0; }
+    fetch_ids(i0 + step);
     T x[kApplyU][V], gg[kApplyU][V], p0[kApplyU][V], p1[kApplyU][V];
     int64_t ev[kApplyU];
     int cv[kApplyU];
@@ -285,14 +307,14 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
     for (int u = 0; u < kApplyU; ++u) {
       const int64_t i = i0 + u * nthreads;
       ok[u] = i < total;
-      const int64_t e = ok[u] ? i / per_edge : 0;
+      const int64_t e = ok[u] ? edge_of(i) : 0;
       const int c = ok[u] ? (int)(i - e * per_edge) * V : 0;
       ev[u] = e;
       cv[u] = c;
-      const int64_t v = __ldg(a.dst + e);
+      const int64_t v = vc[u];
       if constexpr (UV) {
         T xr[V];
-        load_vec<T, V>(static_cast<const T*>(a.el) + (int64_t)__ldg(a.src + e) * a.lde + c, x[u]);
+        load_vec<T, V>(static_cast<const T*>(a.el) + (int64_t)uc[u] * a.lde + c, x[u]);
         load_vec<T, V>(static_cast<const T*>(a.er) + v * a.ldr + c, xr);
 #pragma unroll
         for (int k = 0; k < V; ++k) x[u][k] = x[u][k] + xr[k];

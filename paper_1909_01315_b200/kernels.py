@@ -393,11 +393,68 @@ def gspmm(g, phi, rho, X=None, Y=None, W=None, strategy=None, num_workers=None,
     return _gspmm_launch(g, phi, rho, X, Y, W, d_out, _tuning_struct(strategy))
 
 
+# column tiles for wide gathered operands: 256 B per row slice (64 fp32 / 32 fp64)
+_TILE_BYTES = 256
+_L2_BUDGET = 64 << 20
+
+
+def _tiled_copy_applies(phi, rho, X, d_out, n, tune):
+    """copy_u with sum / mean of a src matrix whose column slices must be
+    L2-tiled (the row kernel's rule) and whose rows are not already aligned
+    256 B runs: pack the tiles so every gather is whole sectors + float4."""
+    if tune is not None or phi.op != "copy_lhs" or phi.lhs_target != "src":
+        return False
+    if rho not in ("sum", "mean") or X is None or X.shape[1] != d_out or n == 0:
+        return False
+    F = X.element_size()
+    tile = _TILE_BYTES // F
+    if d_out <= tile or n * d_out * F <= _L2_BUDGET:
+        return False
+    aligned = _ld(X) % tile == 0 and X.data_ptr() % 16 == 0
+    return not aligned
+
+
+def _gspmm_copy_tiled(g, rho, X, Z, d_out):
+    """copy_u + sum/mean over packed column tiles: gmp_pack_tiles, one
+    gmp_gspmm per 256 B tile (each tile's slice of X stays L2-resident while
+    every destination row gathers it), gmp_unpack_tiles into Z."""
+    lib = _lib.load()
+    dev = g.device
+    n = g.num_nodes
+    F = X.element_size()
+    tile = _TILE_BYTES // F
+    vec = 16 // F
+    nt = -(-d_out // tile)
+    code = _dtype_code(X)
+    stream = _stream(dev)
+    Xp = torch.empty((nt, n, tile), dtype=X.dtype, device=dev)
+    Zp = torch.empty((nt, n, tile), dtype=X.dtype, device=dev)
+    _lib.check(lib.gmp_pack_tiles(n, d_out, code, tile, X.data_ptr(), _ld(X), Xp.data_ptr(),
+                                  stream), "gmp_pack_tiles")
+    adj = g.to_csc()
+    sched = adj.schedule()
+    for t in range(nt):
+        w = min(tile, d_out - t * tile)
+        w = -(-w // vec) * vec  # zero-padded columns keep 16 B vectors
+        lhs = _lib.GmpOperand(Xp[t].data_ptr(), tile, w, _lib.TARGETS["src"])
+        _lib.check(lib.gmp_gspmm(ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct),
+                                 _lib.OPS["copy_lhs"], _lib.RHOS[rho], code, ctypes.byref(lhs),
+                                 None, Zp[t].data_ptr(), tile, w, None, None, None, None, stream),
+                   "gmp_gspmm")
+    _lib.check(lib.gmp_unpack_tiles(n, d_out, code, tile, Zp.data_ptr(), Z.data_ptr(), _ld(Z),
+                                    stream), "gmp_unpack_tiles")
+
+
 def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None):
     lib = _lib.load()
     dev = g.device
     n = g.num_nodes
     ref = next(t for t in (X, Y, W) if t is not None)
+    if _tiled_copy_applies(phi, rho, X, d_out, n, tune):
+        Z = out if out is not None else accounting.register(
+            torch.empty((n, d_out), dtype=ref.dtype, device=dev))
+        _gspmm_copy_tiled(g, rho, X, Z, d_out)
+        return Z, (g.to_csc().degrees().clone() if rho == "mean" else None)
     Z = out if out is not None else accounting.register(
         torch.empty((n, d_out), dtype=ref.dtype, device=dev))
     arg = None

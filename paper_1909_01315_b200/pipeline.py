@@ -42,15 +42,11 @@ def _copy2d(dst, dpitch, src, spitch, width, height, kind, stream):
         raise RuntimeError("cudaMemcpy2DAsync failed with %d" % rc)
 
 
-def tile_bounds(d, n_rows, elem_bytes, l2_budget_mb=64, max_tiles=16):
-    """Column tiles: the widest multiple of 64 columns whose slice of X fits the
-    L2 budget (the row kernel's own rule), at least 2 tiles so copies overlap."""
-    per_col = max(1, n_rows * elem_bytes)
-    fit = max(64, ((l2_budget_mb << 20) // per_col) // 64 * 64)
-    tiles = max(2, min(max_tiles, -(-d // fit)))
-    w = -(-d // tiles)
-    w += w % 2  # keep 8-byte alignment of every tile start for float2 loads
-    return [(c, min(d, c + w)) for c in range(0, d, w)]
+def tile_bounds(d, elem_bytes, tile_bytes=256):
+    """Column tiles of 256 B per row (64 fp32 / 32 fp64 columns) - the row
+    kernel's packed tile width (kernels._gspmm_copy_tiled)."""
+    w = max(1, tile_bytes // elem_bytes)
+    return [(c, min(d, c + w)) for c in range(0, d, w)], w
 
 
 class HostPipeline:
@@ -62,10 +58,10 @@ class HostPipeline:
         self.d2h = torch.cuda.Stream(self.device)
         self.buffers = {}
 
-    def buffer(self, name, shape, dtype):
+    def buffer(self, name, shape, dtype, zero=False):
         b = self.buffers.get(name)
         if b is None or tuple(b.shape) != tuple(shape) or b.dtype != dtype:
-            b = torch.empty(shape, dtype=dtype, device=self.device)
+            b = (torch.zeros if zero else torch.empty)(shape, dtype=dtype, device=self.device)
             self.buffers[name] = b
         return b
 
@@ -73,7 +69,10 @@ class HostPipeline:
 def gspmm_host(g, X_host, Z_host, rho="sum", pipe=None):
     """Z_host = gspmm(g, copy_lhs(src), rho, X_host) with pinned host X_host /
     Z_host (n, d), copies overlapped with the kernel per column tile.
-    Returns Z_host after the copies complete."""
+    The H2D copy of tile t lands packed (n, 64) on the device - the aligned
+    layout the row kernel gathers with 128-bit loads - and the D2H copy
+    scatters the packed output tile back into Z_host's columns, so the tile
+    packing costs no extra pass. Returns Z_host after the copies complete."""
     if rho not in ("sum", "mean"):
         raise ValueError("gspmm_host pipelines copy_u with sum / mean")
     if not (X_host.is_pinned() and Z_host.is_pinned()):
@@ -87,30 +86,32 @@ def gspmm_host(g, X_host, Z_host, rho="sum", pipe=None):
     pipe = pipe or HostPipeline(g.device)
     comp = torch.cuda.current_stream(g.device)
     es = X_host.element_size()
-    Xd = pipe.buffer("X", (n, d), X_host.dtype)
-    Zd = pipe.buffer("Z", (n, d), X_host.dtype)
-    tiles = tile_bounds(d, n, es)
+    tiles, tw = tile_bounds(d, es)
+    vec = max(1, 16 // es)
+    # zero-initialised once: the pad columns of the last tile stay zero
+    Xd = pipe.buffer("X", (len(tiles), n, tw), X_host.dtype, zero=True)
+    Zd = pipe.buffer("Z", (len(tiles), n, tw), X_host.dtype)
     pitch = d * es
     h2d_done, comp_done = [], []
     pipe.h2d.wait_stream(comp)  # buffers are free once earlier work on comp is done
-    for c0, c1 in tiles:
+    for t, (c0, c1) in enumerate(tiles):
         with torch.cuda.stream(pipe.h2d):
-            _copy2d(Xd.data_ptr() + c0 * es, pitch, X_host.data_ptr() + c0 * es, pitch,
+            _copy2d(Xd[t].data_ptr(), tw * es, X_host.data_ptr() + c0 * es, pitch,
                     (c1 - c0) * es, n, _H2D, pipe.h2d)
             ev = torch.cuda.Event()
             ev.record(pipe.h2d)
             h2d_done.append(ev)
     phi = kernels.copy("src")
-    for (c0, c1), ev in zip(tiles, h2d_done):
+    for t, ((c0, c1), ev) in enumerate(zip(tiles, h2d_done)):
         comp.wait_event(ev)
-        kernels._gspmm_launch(g, phi, rho, Xd[:, c0:c1], None, None, c1 - c0,
-                              out=Zd[:, c0:c1])
+        w = -(-(c1 - c0) // vec) * vec
+        kernels._gspmm_launch(g, phi, rho, Xd[t][:, :w], None, None, w, out=Zd[t][:, :w])
         ce = torch.cuda.Event()
         ce.record(comp)
         comp_done.append(ce)
-    for (c0, c1), ce in zip(tiles, comp_done):
+    for t, ((c0, c1), ce) in enumerate(zip(tiles, comp_done)):
         pipe.d2h.wait_event(ce)
-        _copy2d(Z_host.data_ptr() + c0 * es, pitch, Zd.data_ptr() + c0 * es, pitch,
+        _copy2d(Z_host.data_ptr() + c0 * es, pitch, Zd[t].data_ptr(), tw * es,
                 (c1 - c0) * es, n, _D2H, pipe.d2h)
     comp.wait_stream(pipe.d2h)
     return Z_host
