@@ -398,13 +398,23 @@ _TILE_BYTES = 256
 _L2_BUDGET = 64 << 20
 
 
-def _tiled_copy_applies(phi, rho, X, d_out, n, tune):
-    """copy_u with sum / mean of a src matrix whose column slices must be
-    L2-tiled (the row kernel's rule) and whose rows are not already aligned
-    256 B runs: pack the tiles so every gather is whole sectors + float4."""
-    if tune is not None or phi.op != "copy_lhs" or phi.lhs_target != "src":
+def _tiled_applies(phi, rho, X, W, d_out, n, tune):
+    """Wide src-gathered aggregations whose column slices must be L2-tiled
+    (the row kernel's rule) and whose rows are not already aligned 256 B runs:
+    copy_u, or u_op_e with a per-edge scalar (the attention-weighted sum),
+    under sum / mean. Packing the tiles makes every gather whole sectors read
+    with 128-bit loads."""
+    if tune is not None or rho not in ("sum", "mean") or X is None or n == 0:
         return False
-    if rho not in ("sum", "mean") or X is None or X.shape[1] != d_out or n == 0:
+    if phi.op == "copy_lhs":
+        if phi.lhs_target != "src":
+            return False
+    elif phi.op in ("add", "sub", "mul", "div"):
+        if (phi.lhs_target, phi.rhs_target) != ("src", "edge") or W is None or W.shape[1] != 1:
+            return False
+    else:
+        return False
+    if X.shape[1] != d_out:
         return False
     F = X.element_size()
     tile = _TILE_BYTES // F
@@ -414,10 +424,11 @@ def _tiled_copy_applies(phi, rho, X, d_out, n, tune):
     return not aligned
 
 
-def _gspmm_copy_tiled(g, rho, X, Z, d_out):
-    """copy_u + sum/mean over packed column tiles: gmp_pack_tiles, one
-    gmp_gspmm per 256 B tile (each tile's slice of X stays L2-resident while
-    every destination row gathers it), gmp_unpack_tiles into Z."""
+def _gspmm_tiled(g, phi, rho, X, W, Z, d_out):
+    """Aggregation over packed column tiles: gmp_pack_tiles, one gmp_gspmm per
+    256 B tile (each tile's slice of X stays L2-resident while every
+    destination row gathers it; a per-edge scalar is laid out in CSC order
+    once and streamed by every tile), gmp_unpack_tiles into Z."""
     lib = _lib.load()
     dev = g.device
     n = g.num_nodes
@@ -427,22 +438,36 @@ def _gspmm_copy_tiled(g, rho, X, Z, d_out):
     nt = -(-d_out // tile)
     code = _dtype_code(X)
     stream = _stream(dev)
+    adj = g.to_csc()
+    sched = adj.schedule()
+    rhs = None
+    err = None
+    if phi.op != "copy_lhs":
+        Wc = _gather_rows(adj.edge_ids, W.to(X.dtype))
+        rhs = _lib.GmpOperand(_data_ptr(Wc), 1, 1, _lib.TARGETS["edge_pos"])
+        if phi.op == "div":
+            err = _err_slot(dev)
     Xp = torch.empty((nt, n, tile), dtype=X.dtype, device=dev)
     Zp = torch.empty((nt, n, tile), dtype=X.dtype, device=dev)
     _lib.check(lib.gmp_pack_tiles(n, d_out, code, tile, X.data_ptr(), _ld(X), Xp.data_ptr(),
                                   stream), "gmp_pack_tiles")
-    adj = g.to_csc()
-    sched = adj.schedule()
     for t in range(nt):
         w = min(tile, d_out - t * tile)
         w = -(-w // vec) * vec  # zero-padded columns keep 16 B vectors
         lhs = _lib.GmpOperand(Xp[t].data_ptr(), tile, w, _lib.TARGETS["src"])
+        if rhs is not None:
+            rhs.dim = 1
         _lib.check(lib.gmp_gspmm(ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct),
-                                 _lib.OPS["copy_lhs"], _lib.RHOS[rho], code, ctypes.byref(lhs),
-                                 None, Zp[t].data_ptr(), tile, w, None, None, None, None, stream),
+                                 _lib.OPS[phi.op], _lib.RHOS[rho], code, ctypes.byref(lhs),
+                                 _ptr(rhs), Zp[t].data_ptr(), tile, w, None, None,
+                                 err.data_ptr() if err is not None else None, None, stream),
                    "gmp_gspmm")
     _lib.check(lib.gmp_unpack_tiles(n, d_out, code, tile, Zp.data_ptr(), Z.data_ptr(), _ld(Z),
                                     stream), "gmp_unpack_tiles")
+    if err is not None:
+        pos = int(err.item())
+        if pos != _INT32_MAX:
+            _raise_div_zero(adj.edge_ids[pos].item())
 
 
 def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None):
@@ -450,10 +475,10 @@ def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None):
     dev = g.device
     n = g.num_nodes
     ref = next(t for t in (X, Y, W) if t is not None)
-    if _tiled_copy_applies(phi, rho, X, d_out, n, tune):
+    if _tiled_applies(phi, rho, X, W, d_out, n, tune):
         Z = out if out is not None else accounting.register(
             torch.empty((n, d_out), dtype=ref.dtype, device=dev))
-        _gspmm_copy_tiled(g, rho, X, Z, d_out)
+        _gspmm_tiled(g, phi, rho, X, W, Z, d_out)
         return Z, (g.to_csc().degrees().clone() if rho == "mean" else None)
     Z = out if out is not None else accounting.register(
         torch.empty((n, d_out), dtype=ref.dtype, device=dev))

@@ -44,7 +44,7 @@ def _copy2d(dst, dpitch, src, spitch, width, height, kind, stream):
 
 def tile_bounds(d, elem_bytes, tile_bytes=256):
     """Column tiles of 256 B per row (64 fp32 / 32 fp64 columns) - the row
-    kernel's packed tile width (kernels._gspmm_copy_tiled)."""
+    kernel's packed tile width (kernels._gspmm_tiled)."""
     w = max(1, tile_bytes // elem_bytes)
     return [(c, min(d, c + w)) for c in range(0, d, w)], w
 

@@ -75,3 +75,33 @@ def test_host_pipeline_packed_tiles(d):
         torch.cuda.synchronize()
         want, _ = O.gspmm(s, dd, n, "copy_lhs", "src", None, rho, X=x.astype(np.float64))
         assert np.allclose(zh.numpy(), want, rtol=RTOL32, atol=ATOL32)
+
+
+@pytest.mark.parametrize("op", ["mul", "add", "sub", "div"])
+@pytest.mark.parametrize("rho", ["sum", "mean"])
+def test_tiled_u_op_e_scalar_matches_oracle(small_budget, op, rho):
+    s, dd, n = graph()
+    g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((n, 150)).astype(np.float32)
+    w = (np.abs(rng.standard_normal((s.size, 1))) + 0.5).astype(np.float32)
+    Z, _ = G.gspmm(g, kernels.MessageFunc(op, "src", "edge"), rho,
+                   X=torch.as_tensor(x, device=DEV), W=torch.as_tensor(w, device=DEV))
+    want, _ = O.gspmm(s, dd, n, op, "src", "edge", rho, X=x.astype(np.float64),
+                      W=w.astype(np.float64))
+    assert np.allclose(to_np(Z), want, rtol=RTOL32, atol=ATOL32)
+
+
+def test_tiled_div_by_zero_names_smallest_edge(small_budget):
+    s, dd, n = graph()
+    g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
+    w = torch.ones((s.size, 1), device=DEV)
+    zeros = [17, 5000, 9]
+    w[zeros] = 0.0
+    # the reference walks the in-adjacency (kernels.py:263-268, 473-482): the
+    # zero divisor met first in CSC order is named
+    eids = to_np(g.to_csc().edge_ids)
+    first = int(eids[min(int(np.flatnonzero(eids == z)[0]) for z in zeros)])
+    with pytest.raises(ZeroDivisionError, match="edge id %d$" % first):
+        G.gspmm(g, kernels.MessageFunc("div", "src", "edge"), "sum",
+                X=torch.ones((n, 150), device=DEV), W=w)
