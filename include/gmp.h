@@ -62,7 +62,11 @@ typedef struct {
  * have degree > heavy_threshold and are reduced by a whole CTA; rows
  * order[n_heavy..n_medium) (degree > light_threshold) by one warp each; the
  * rest (short rows, then empty rows) several per warp, one per lane group.
- * order == NULL means identity order, every row on the warp path. */
+ * order == NULL means identity order, every row on the warp path.
+ * sorted_eids (nullable): the adjacency's edge ids with each row's ids in
+ * ascending order (equal to eids when they already ascend inside rows); when
+ * given, edge-keyed passes over heavy rows (edge_softmax statistics) run in
+ * L2-sized edge-id windows. */
 typedef struct {
   const int32_t* order;
   int64_t n_heavy;
@@ -70,6 +74,7 @@ typedef struct {
   int64_t n_nonempty;
   int32_t heavy_threshold;
   int32_t light_threshold;
+  const int32_t* sorted_eids;
 } gmp_sched;
 
 /* COO edge list in edge-id order (graph.py:98-100). */
@@ -154,6 +159,10 @@ int gmp_gsddmm(const gmp_coo* coo, int op, int dtype,
  * workspace: gmp_edge_softmax_workspace_size(n_rows, H) bytes of device
  * memory for the per-destination statistics. */
 size_t gmp_edge_softmax_workspace_size(int64_t n_rows, int32_t H);
+/* Workspace that also enables the windowed statistics pass (sched->sorted_eids
+ * set, heavy rows present, large edge count); >= the plain size. */
+size_t gmp_edge_softmax_workspace_size_ex(const gmp_adj* in_adj, const gmp_sched* sched, int32_t H,
+                                          int dtype, int backward);
 
 int gmp_edge_softmax_fwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sched* sched,
                          int dtype, const void* scores, int64_t lds, int32_t H,

@@ -20,7 +20,7 @@ RHOS = {"sum": 0, "max": 1, "min": 2, "mean": 3}
 GMP_F32, GMP_F64 = 0, 1
 
 EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "gmp_gsddmm",
-            "gmp_edge_softmax_workspace_size", "gmp_edge_softmax_fwd", "gmp_edge_softmax_uv_fwd", "gmp_edge_softmax_bwd", "gmp_route_extrema",
+            "gmp_edge_softmax_workspace_size", "gmp_edge_softmax_workspace_size_ex", "gmp_edge_softmax_fwd", "gmp_edge_softmax_uv_fwd", "gmp_edge_softmax_bwd", "gmp_route_extrema",
             "gmp_extrema_bwd_copy", "gmp_gather_rows", "gmp_neighbor_sample",
             "gmp_edge_softmax_uv_stats", "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
             "gmp_version")
@@ -35,7 +35,8 @@ class GmpAdj(ctypes.Structure):
 class GmpSched(ctypes.Structure):
     _fields_ = [("order", ctypes.c_void_p), ("n_heavy", ctypes.c_int64),
                 ("n_medium", ctypes.c_int64), ("n_nonempty", ctypes.c_int64),
-                ("heavy_threshold", ctypes.c_int32), ("light_threshold", ctypes.c_int32)]
+                ("heavy_threshold", ctypes.c_int32), ("light_threshold", ctypes.c_int32),
+                ("sorted_eids", ctypes.c_void_p)]
 
 
 class GmpCoo(ctypes.Structure):
@@ -76,6 +77,8 @@ def _declare(lib):
                                vp, i64, i32, vp, vp]
     lib.gmp_edge_softmax_workspace_size.argtypes = [i64, i32]
     lib.gmp_edge_softmax_workspace_size.restype = ctypes.c_size_t
+    lib.gmp_edge_softmax_workspace_size_ex.argtypes = [_P(GmpAdj), _P(GmpSched), i32, c_int, c_int]
+    lib.gmp_edge_softmax_workspace_size_ex.restype = ctypes.c_size_t
     lib.gmp_edge_softmax_fwd.argtypes = [_P(GmpAdj), _P(GmpCoo), _P(GmpSched), c_int, vp, i64, i32,
                                          vp, i64, vp, ctypes.c_size_t, vp]
     lib.gmp_edge_softmax_uv_fwd.argtypes = [_P(GmpAdj), _P(GmpCoo), _P(GmpSched), c_int, vp, i64,

@@ -30,6 +30,7 @@ cudaError_t launch_pack_tiles(int, bool, int64_t, int32_t, int32_t, const void*,
                               int64_t, cudaStream_t);
 cudaError_t launch_neighbor_sample(const int64_t*, const int64_t*, int64_t, const int64_t*, uint64_t,
                                    int64_t*, int64_t*, cudaStream_t);
+int softmax_window_resident_ctas(int f64, int V, bool bwd);
 cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t light,
                            int32_t* order_out, void* ws, size_t ws_bytes, int64_t* n_heavy,
                            int64_t* n_medium, int64_t* n_nonempty, cudaStream_t s);
@@ -432,6 +433,56 @@ size_t gmp_edge_softmax_workspace_size(int64_t n_rows, int32_t H) {
   return (size_t)std::max<int64_t>(0, n_rows) * (size_t)std::max(0, H) * 2 * sizeof(double);
 }
 
+// Windowed statistics plan: windows of `win` edge ids whose score rows (both
+// operands for the backward) of all in-flight windows fit an L2 budget.
+struct WindowPlan {
+  bool on;
+  int64_t win, n_windows;
+  size_t off_counter, off_pm, off_pl, off_bounds, bytes;
+};
+
+static WindowPlan window_plan(const gmp_adj* adj, const gmp_sched* sched, int32_t H, size_t F,
+                              bool bwd, int V) {
+  WindowPlan p{};
+  const size_t base = gmp_edge_softmax_workspace_size(adj ? adj->n_rows : 0, H);
+  p.bytes = base;
+  if (!adj || !sched || !sched->sorted_eids || sched->n_heavy <= 0 || H <= 0 || H > 32 * V ||
+      adj->m < (1 << 22))
+    return p;
+  const int64_t R = sched->n_heavy;
+  const int64_t warps = (int64_t)softmax_window_resident_ctas(F == 8, V, bwd) * kWarpsPerCta;
+  const int64_t inflight = (warps + R - 1) / R + 1;  // windows touched by the warps in flight
+  const int64_t row_bytes = (int64_t)H * (int64_t)F * (bwd ? 2 : 1);
+  const int64_t budget = 80ll << 20;
+  const int64_t win = budget / (inflight * row_bytes);
+  if (win < (1 << 15)) return p;
+  p.win = win;
+  p.n_windows = (adj->m + win - 1) / win;
+  const size_t part = (size_t)p.n_windows * (size_t)R * (size_t)H;
+  p.off_counter = (base + 255) / 256 * 256;
+  p.off_pm = p.off_counter + 256;
+  p.off_pl = (p.off_pm + part * F + 255) / 256 * 256;
+  p.off_bounds = (p.off_pl + part * sizeof(double) + 255) / 256 * 256;
+  p.bytes = p.off_bounds + (size_t)R * (size_t)(p.n_windows + 1) * sizeof(int64_t);
+  p.on = true;
+  return p;
+}
+
+static int softmax_vec(size_t F, int32_t H) {
+  const int cands[3] = {4, 2, 1};
+  for (int V : cands) {
+    if (F == 8 && V == 4) continue;
+    if (H % V == 0) return V;
+  }
+  return 1;
+}
+
+size_t gmp_edge_softmax_workspace_size_ex(const gmp_adj* in_adj, const gmp_sched* sched, int32_t H,
+                                          int dtype, int backward) {
+  const size_t F = dtype == GMP_F64 ? 8 : 4;
+  return window_plan(in_adj, sched, H, F, backward != 0, softmax_vec(F, H)).bytes;
+}
+
 static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sched* sched,
                           int dtype, const void* s, int64_t lds, const void* g, int64_t ldg,
                           int32_t H, void* out, int64_t ldo, void* ws, size_t ws_bytes, bool bwd,
@@ -472,8 +523,33 @@ static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sche
   a.stat = ws;
   a.el = el; a.lde = lde; a.er = er; a.ldr = ldr; a.src = coo ? coo->src : nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = launch_edge_softmax(F == 8, V, bwd, uv, a, a.blocks_per_tile * ntiles, st);
-  g_launches++;
+  cudaError_t e;
+  const WindowPlan wp = uv ? WindowPlan{} : window_plan(adj, sched, H, F, bwd, V);
+  if (wp.on && ntiles == 1 && V == softmax_vec(F, H) && ws_bytes >= wp.bytes) {
+    // heavy rows: edge-id windows; the rest: the row kernel on the light rows
+    WindowArgs w{};
+    w.sorted_eids = sched->sorted_eids;
+    w.win = wp.win;
+    w.n_windows = wp.n_windows;
+    w.counter = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + wp.off_counter);
+    w.pm = static_cast<char*>(ws) + wp.off_pm;
+    w.pl = reinterpret_cast<double*>(static_cast<char*>(ws) + wp.off_pl);
+    w.bounds = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + wp.off_bounds);
+    e = launch_edge_softmax_window(F == 8, V, bwd, a, w, st);
+    g_launches += 3;
+    SoftmaxArgs lt = a;
+    lt.order = a.order + n_heavy;
+    lt.n_rows = adj->n_rows - n_heavy;
+    lt.n_heavy = 0;
+    lt.blocks_per_tile = (lt.n_rows + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (e == cudaSuccess && lt.n_rows > 0) {
+      e = launch_edge_softmax(F == 8, V, bwd, uv, lt, lt.blocks_per_tile, st);
+      g_launches++;
+    }
+  } else {
+    e = launch_edge_softmax(F == 8, V, bwd, uv, a, a.blocks_per_tile * ntiles, st);
+    g_launches++;
+  }
   if (e == cudaSuccess && !stats_only) {
     e = launch_edge_softmax_apply(F == 8, V, bwd, uv, a, st);
     g_launches++;

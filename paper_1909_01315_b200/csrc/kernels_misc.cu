@@ -99,6 +99,68 @@ cudaError_t launch_edge_softmax(int f64, int V, bool bwd, bool uv, const Softmax
   return cudaGetLastError();
 }
 
+template <typename T, bool BWD>
+static void softmax_window_v(int V, const SoftmaxArgs& a, const WindowArgs& w, unsigned grid,
+                             cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {
+    if (V == 4) { edge_softmax_window_kernel<T, 4, BWD><<<grid, kWarpsPerCta * 32, 0, s>>>(a, w); return; }
+  }
+  if (V == 2) { edge_softmax_window_kernel<T, 2, BWD><<<grid, kWarpsPerCta * 32, 0, s>>>(a, w); return; }
+  edge_softmax_window_kernel<T, 1, BWD><<<grid, kWarpsPerCta * 32, 0, s>>>(a, w);
+}
+
+// resident warps of the window kernel on this device (for window sizing)
+int softmax_window_resident_ctas(int f64, int V, bool bwd) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fn;
+  if (f64) {
+    fn = bwd ? (V == 2 ? (const void*)edge_softmax_window_kernel<double, 2, true>
+                       : (const void*)edge_softmax_window_kernel<double, 1, true>)
+             : (V == 2 ? (const void*)edge_softmax_window_kernel<double, 2, false>
+                       : (const void*)edge_softmax_window_kernel<double, 1, false>);
+  } else {
+    fn = bwd ? (V == 4 ? (const void*)edge_softmax_window_kernel<float, 4, true>
+                       : V == 2 ? (const void*)edge_softmax_window_kernel<float, 2, true>
+                                : (const void*)edge_softmax_window_kernel<float, 1, true>)
+             : (V == 4 ? (const void*)edge_softmax_window_kernel<float, 4, false>
+                       : V == 2 ? (const void*)edge_softmax_window_kernel<float, 2, false>
+                                : (const void*)edge_softmax_window_kernel<float, 1, false>);
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kWarpsPerCta * 32, 0);
+  return std::max(1, per) * sms;
+}
+
+cudaError_t launch_edge_softmax_window(int f64, int V, bool bwd, const SoftmaxArgs& a,
+                                       const WindowArgs& w, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  {
+    const int64_t nb = a.n_heavy * (w.n_windows + 1);
+    edge_softmax_window_bounds<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + 255) / 256, 148 * 16)),
+                                 256, 0, s>>>(a, w);
+  }
+  const unsigned grid = (unsigned)softmax_window_resident_ctas(f64, V, bwd);
+  if (f64) {
+    if (bwd) softmax_window_v<double, true>(V, a, w, grid, s);
+    else softmax_window_v<double, false>(V, a, w, grid, s);
+  } else {
+    if (bwd) softmax_window_v<float, true>(V, a, w, grid, s);
+    else softmax_window_v<float, false>(V, a, w, grid, s);
+  }
+  const int64_t total = a.n_heavy * (int64_t)a.H;  // one warp each
+  const unsigned mg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 7) / 8, 148 * 16));
+  if (f64) {
+    if (bwd) edge_softmax_window_merge<double, true><<<mg, 256, 0, s>>>(a, w);
+    else edge_softmax_window_merge<double, false><<<mg, 256, 0, s>>>(a, w);
+  } else {
+    if (bwd) edge_softmax_window_merge<float, true><<<mg, 256, 0, s>>>(a, w);
+    else edge_softmax_window_merge<float, false><<<mg, 256, 0, s>>>(a, w);
+  }
+  return cudaGetLastError();
+}
+
 template <typename T, bool BWD, bool UV>
 static void softmax_apply_v(int V, const SoftmaxArgs& a, cudaStream_t s) {
   const int64_t total = a.m * (int64_t)(a.H / V);

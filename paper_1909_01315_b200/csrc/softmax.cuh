@@ -58,16 +58,30 @@ struct SoftmaxArgs {
   const int32_t* src;  // COO sources (apply kernel, fused mode)
 };
 
-__device__ __forceinline__ float exp_t(float x) { return expf(x); }
-__device__ __forceinline__ double exp_t(double x) { return exp(x); }
+
+// exp(x - m) of a softmax term. fp32: 2^((x - m) log2 e) on the SFU
+// (ex2.approx.ftz, max rel. error 2^-22; the FFMA-formed argument adds
+// |x - m| * 2^-24 relative - below 1e-6 for any term >= 1e-6 of its row's
+// max, results below 2^-126 flush to zero). Every fp32 softmax term in the
+// library (statistics, normalisation, fused GAT weights) uses this one
+// formula, so a row's weights sum to 1 up to the rounding of the terms.
+constexpr float kLog2e = 1.4426950408889634f;
+__device__ __forceinline__ float softmax_exp(float x, float m) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmaf_rn(x, kLog2e, -m * kLog2e)));
+  return y;
+}
+__device__ __forceinline__ double softmax_exp(double x, double m) { return exp(x - m); }
 
 // (m, l) online-softmax merge in fp64 for l; empty partials carry m = -inf.
 template <typename T>
 __device__ __forceinline__ void sm_merge(T& m, double& l, T om, double ol) {
   if (om == -INFINITY) return;
   if (m == -INFINITY) { m = om; l = ol; return; }
-  if (om > m) { l = l * exp((double)m - (double)om) + ol; m = om; }
-  else        { l += ol * exp((double)om - (double)m); }
+  // the rescale factor in the element precision: its error (~1 ulp of the
+  // fp32 exponent difference) is weighted by the factor itself, < 3e-8 of l
+  if (om > m) { l = l * (double)softmax_exp(m, om) + ol; m = om; }
+  else        { l += ol * (double)softmax_exp(om, m); }
 }
 
 // per-column running sum: compensated fp32 pair for float, plain fp64 for double
@@ -97,53 +111,31 @@ template <> struct ColSum<double> {
 // one warp step.
 constexpr int kChunk = 256;
 
+template <int V>
+struct StatsUnroll {
+  static constexpr int value = V == 4 ? 4 : 8;
+};
+
+// Pass 1 of the statistics for edges [pb, pe) of one row owned by this warp
+// (chunks pb + first, + stride, ...): online (max, sum exp) per column (fwd)
+// or sum alpha * g (bwd). ids: edge ids (UV: source node ids).
 template <typename T, int V, bool BWD, bool UV>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const SoftmaxArgs a) {
-  constexpr int U = V == 4 ? 4 : 8;
+__device__ __forceinline__ void stats_pass1(const SoftmaxArgs& a, const int32_t* __restrict__ ids,
+                                            int64_t pb, int64_t pe, int64_t first,
+                                            int64_t stride, int lane, int slot, int E, bool valid,
+                                            int ccol, const T (&er_row)[V], int32_t* buf,
+                                            T (&m)[V], ColSum<T> (&acc)[V]) {
+  constexpr int U = StatsUnroll<V>::value;
   constexpr int B = kChunk / 32;
-  __shared__ double s_l[kWarpsPerCta][32 * V];
-  __shared__ T s_m[kWarpsPerCta][32 * V];
-  __shared__ int32_t s_eid[kWarpsPerCta][kChunk];
-  const int64_t bid = blockIdx.x;
-  const int tile = (int)(bid / a.blocks_per_tile);
-  const int64_t local = bid - (int64_t)tile * a.blocks_per_tile;
-  const int c0 = tile * a.tile_cols, c1 = min(a.H, c0 + a.tile_cols);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = 1 << a.g_log2, E = 32 >> a.g_log2;
-  const int slot = lane >> a.g_log2, gl = lane & (G - 1);
-  const bool heavy = local < a.n_heavy;
-  int64_t row;
-  if (heavy) {
-    row = a.order[local];
-  } else {
-    const int64_t r = a.n_heavy + (local - a.n_heavy) * kWarpsPerCta + warp;
-    if (r >= a.n_rows) return;
-    row = a.order ? (int64_t)a.order[r] : r;
-  }
-  const int64_t pb = a.indptr[row], pe = a.indptr[row + 1];
-  if (pe == pb) return;  // no in-edges: nothing keyed to this row (heavy rows are never empty)
-  const int col = c0 + gl * V;
-  const bool valid = col < c1;
-  const int ccol = valid ? col : 0;
   const T* S = static_cast<const T*>(a.s) + ccol;
   const T* Gd = static_cast<const T*>(a.g) + ccol;
   const T* EL = UV ? static_cast<const T*>(a.el) + ccol : nullptr;
-  T er_row[V];
-#pragma unroll
-  for (int k = 0; k < V; ++k) er_row[k] = T(0);
-  if (UV) load_vec<T, V>(static_cast<const T*>(a.er) + row * a.ldr + ccol, er_row);
-  T* O = static_cast<T*>(a.out) + ccol;
-  const int64_t first = heavy ? (int64_t)warp * kChunk : 0;
-  const int64_t stride = heavy ? (int64_t)kChunk * kWarpsPerCta : kChunk;
-  int32_t* buf = s_eid[warp];
-
-  // stage chunk `cb` of edge ids into this warp's buffer (prefetched registers)
   int32_t pre[B];
   auto fetch = [&](int64_t cb) {
 #pragma unroll
     for (int i = 0; i < B; ++i) {
       const int64_t q = cb + i * 32 + lane;
-      pre[i] = q < pe ? __ldg((UV ? a.indices : a.eids) + q) : 0;
+      pre[i] = q < pe ? __ldg(ids + q) : 0;
     }
   };
   auto stage = [&]() {
@@ -152,12 +144,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
     for (int i = 0; i < B; ++i) buf[i * 32 + lane] = pre[i];
     __syncwarp();
   };
-
-  // ---- pass 1: online max + sum (fwd) / sum of alpha * g (bwd) ----
-  T m[V];
-  ColSum<T> acc[V];
-#pragma unroll
-  for (int k = 0; k < V; ++k) m[k] = -INFINITY;
   fetch(pb + first);
   for (int64_t cb = pb + first; cb < pe; cb += stride) {
     const int cnt = (int)min((int64_t)kChunk, pe - cb);
@@ -182,27 +168,38 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
           if constexpr (BWD) load_vec<T, V>(Gd + e * a.ldg, gg[u]);
         }
       }
+      if constexpr (BWD) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (!ok[u]) continue;
+        for (int u = 0; u < U; ++u) {
+          if (!ok[u]) continue;
+#pragma unroll
+          for (int k = 0; k < V; ++k) acc[k].add_prod(x[u][k], gg[u][k]);
+        }
+      } else {
+        // one rescale per group of U edges: the group max first, then one
+        // exp per element relative to the (possibly raised) running max
 #pragma unroll
         for (int k = 0; k < V; ++k) {
-          if constexpr (BWD) {
-            acc[k].add_prod(x[u][k], gg[u][k]);
-          } else {
-            if (x[u][k] > m[k]) {
-              acc[k].scale(exp_t(T(m[k] - x[u][k])));
-              m[k] = x[u][k];
-            }
-            acc[k].add(exp_t(T(x[u][k] - m[k])));
+          T mx = m[k];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u] && x[u][k] > mx) mx = x[u][k];
+          if (mx > m[k]) {
+            if (m[k] != T(-INFINITY)) acc[k].scale(softmax_exp(m[k], mx));
+            m[k] = mx;
           }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) acc[k].add(softmax_exp(x[u][k], m[k]));
         }
       }
     }
   }
-  double l[V];
-#pragma unroll
-  for (int k = 0; k < V; ++k) l[k] = acc[k].value();
+}
+
+// fold the slots of a warp: every lane group ends with its columns' (m, l)
+template <typename T, int V, bool BWD>
+__device__ __forceinline__ void stats_warp_combine(int G, T (&m)[V], double (&l)[V]) {
   for (int off = G; off < 32; off <<= 1) {
 #pragma unroll
     for (int k = 0; k < V; ++k) {
@@ -215,6 +212,68 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
       }
     }
   }
+}
+
+template <typename T, int V, bool BWD>
+__device__ __forceinline__ void stats_write(const SoftmaxArgs& a, int64_t row, int col,
+                                            const T (&m)[V], const double (&l)[V]) {
+  T* st = static_cast<T*>(a.stat) + row * 2 * (int64_t)a.H + col;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    if constexpr (BWD) {
+      const T hi = (T)l[k];
+      st[k] = hi;
+      st[a.H + k] = (T)(l[k] - (double)hi);
+    } else {
+      st[k] = m[k];
+      st[a.H + k] = (T)(1.0 / l[k]);
+    }
+  }
+}
+
+template <typename T, int V, bool BWD, bool UV>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const SoftmaxArgs a) {
+  __shared__ double s_l[kWarpsPerCta][32 * V];
+  __shared__ T s_m[kWarpsPerCta][32 * V];
+  __shared__ int32_t s_eid[kWarpsPerCta][kChunk];
+  const int64_t bid = blockIdx.x;
+  const int tile = (int)(bid / a.blocks_per_tile);
+  const int64_t local = bid - (int64_t)tile * a.blocks_per_tile;
+  const int c0 = tile * a.tile_cols, c1 = min(a.H, c0 + a.tile_cols);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = 1 << a.g_log2, E = 32 >> a.g_log2;
+  const int slot = lane >> a.g_log2, gl = lane & (G - 1);
+  const bool heavy = local < a.n_heavy;
+  int64_t row;
+  if (heavy) {
+    row = a.order[local];
+  } else {
+    const int64_t r = a.n_heavy + (local - a.n_heavy) * kWarpsPerCta + warp;
+    if (r >= a.n_rows) return;
+    row = a.order ? (int64_t)a.order[r] : r;
+  }
+  const int64_t pb = a.indptr[row], pe = a.indptr[row + 1];
+  if (pe == pb) return;  // no in-edges: nothing keyed to this row (heavy rows are never empty)
+  const int col = c0 + gl * V;
+  const bool valid = col < c1;
+  const int ccol = valid ? col : 0;
+  T er_row[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) er_row[k] = T(0);
+  if (UV) load_vec<T, V>(static_cast<const T*>(a.er) + row * a.ldr + ccol, er_row);
+
+  T m[V];
+  ColSum<T> acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) m[k] = -INFINITY;
+  stats_pass1<T, V, BWD, UV>(a, UV ? a.indices : a.eids, pb, pe,
+                             heavy ? (int64_t)warp * kChunk : 0,
+                             heavy ? (int64_t)kChunk * kWarpsPerCta : kChunk, lane, slot, E,
+                             valid, ccol, er_row, s_eid[warp], m, acc);
+  double l[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) l[k] = acc[k].value();
+  stats_warp_combine<T, V, BWD>(G, m, l);
   if (heavy) {
     if (slot == 0) {
 #pragma unroll
@@ -238,26 +297,131 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
 #pragma unroll
     for (int k = 0; k < V; ++k) { m[k] = s_m[0][gl * V + k]; l[k] = s_l[0][gl * V + k]; }
   }
-  // every slot of the warp needs its lane-group's final (m, l)
-#pragma unroll
-  for (int k = 0; k < V; ++k) {
-    l[k] = __shfl_sync(kFull, l[k], gl);
-    m[k] = __shfl_sync(kFull, m[k], gl);
-  }
+  if (slot == 0 && valid) stats_write<T, V, BWD>(a, row, col, m, l);
+}
 
-  // ---- per-destination statistics: (max, 1/sum) fwd, (sum_hi, sum_lo) bwd ----
-  if (slot == 0 && valid) {
-    T* st = static_cast<T*>(a.stat) + row * 2 * (int64_t)a.H + col;
+// Windowed statistics for the heavy rows (edge-keyed scores only). A random
+// 32 B score row costs a whole 128 B DRAM line (tools/micro/randread.cu), so
+// walking heavy rows in CSC order moves ~4x the score bytes. Instead the edge
+// ids are cut into windows of `win` consecutive ids whose score rows fit in L2
+// together, and work items (window b, heavy row r) - the part of row r's
+// edge list (ascending edge ids, `sorted_eids`) inside window b - are handed
+// out in window-major order through an atomic counter, so the warps in flight
+// share one or two windows and every score line is fetched from DRAM about
+// once. Each item writes a partial (max, sum) per column; a merge kernel
+// combines a row's partials in window order (deterministic).
+struct WindowArgs {
+  const int32_t* sorted_eids;  // in-adjacency edge ids, ascending inside each row
+  int64_t win;                 // edge ids per window
+  int64_t n_windows;
+  unsigned long long* counter; // work-item counter (zeroed by the launcher)
+  int64_t* bounds;             // (n_heavy, n_windows + 1): first position of each window in a row
+  void* pm;                    // (n_windows, n_heavy, H) T: partial max (fwd)
+  double* pl;                  // (n_windows, n_heavy, H): partial sum
+};
+
+template <typename T, int V, bool BWD>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    edge_softmax_window_kernel(const SoftmaxArgs a, const WindowArgs w) {
+  __shared__ int32_t s_eid[kWarpsPerCta][kChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = 1 << a.g_log2, E = 32 >> a.g_log2;
+  const int slot = lane >> a.g_log2, gl = lane & (G - 1);
+  const int col = gl * V;  // one column tile (H <= 32 V)
+  const bool valid = col < a.H;
+  const int ccol = valid ? col : 0;
+  const int64_t items = w.n_windows * a.n_heavy;
+  T zero_row[V];
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      if constexpr (BWD) {
-        const T hi = (T)l[k];
-        st[k] = hi;
-        st[a.H + k] = (T)(l[k] - (double)hi);
-      } else {
-        st[k] = m[k];
-        st[a.H + k] = (T)(1.0 / l[k]);
+  for (int k = 0; k < V; ++k) zero_row[k] = T(0);
+  // the next item's index is claimed one item ahead (hides the atomic's latency)
+  unsigned long long nxt = 0;
+  if (lane == 0) nxt = atomicAdd(w.counter, 1ull);
+  for (;;) {
+    const unsigned long long it = __shfl_sync(kFull, nxt, 0);
+    if ((int64_t)it >= items) return;
+    if (lane == 0) nxt = atomicAdd(w.counter, 1ull);
+    const int64_t b = (int64_t)it / a.n_heavy, r = (int64_t)it - b * a.n_heavy;
+    // [lo, hi): positions of row r's edge ids inside [b*win, (b+1)*win)
+    const int64_t* bd = w.bounds + r * (w.n_windows + 1) + b;
+    const int64_t lo = __ldg(bd), hi = __ldg(bd + 1);
+    T m[V];
+    ColSum<T> acc[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) m[k] = -INFINITY;
+    if (hi > lo)
+      stats_pass1<T, V, BWD, false>(a, w.sorted_eids, lo, hi, 0, kChunk, lane, slot, E, valid,
+                                    ccol, zero_row, s_eid[warp], m, acc);
+    double l[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) l[k] = acc[k].value();
+    stats_warp_combine<T, V, BWD>(G, m, l);
+    if (slot == 0 && valid) {
+      const int64_t base = ((int64_t)b * a.n_heavy + r) * a.H + col;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if constexpr (!BWD) static_cast<T*>(w.pm)[base + k] = m[k];
+        w.pl[base + k] = l[k];
       }
+    }
+  }
+}
+
+// bounds[r][b] = first position p in heavy row r with sorted_eids[p] >= b*win
+// (b = 0..n_windows): one independent binary search per thread
+static __global__ void edge_softmax_window_bounds(const SoftmaxArgs a, const WindowArgs w) {
+  const int64_t per = w.n_windows + 1;
+  const int64_t total = a.n_heavy * per;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per, b = i - r * per;
+    const int64_t row = a.order[r];
+    int64_t x = a.indptr[row], y = a.indptr[row + 1];
+    const int64_t e0 = b * w.win;
+    while (x < y) {
+      const int64_t mid = (x + y) >> 1;
+      if (__ldg(w.sorted_eids + mid) < e0) x = mid + 1; else y = mid;
+    }
+    w.bounds[i] = x;
+  }
+}
+
+// one warp per (heavy row, column): lanes merge strided window partials,
+// then a fixed xor tree combines the lanes (deterministic)
+template <typename T, bool BWD>
+__global__ void edge_softmax_window_merge(const SoftmaxArgs a, const WindowArgs w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = a.n_heavy * (int64_t)a.H;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nw) {
+    const int64_t r = i / a.H;
+    const int c = (int)(i - r * a.H);
+    T mm = -INFINITY;
+    double ll = 0.0;
+    for (int64_t b = lane; b < w.n_windows; b += 32) {
+      const int64_t at = (b * a.n_heavy + r) * a.H + c;
+      if constexpr (BWD) ll += w.pl[at];
+      else sm_merge<T>(mm, ll, static_cast<const T*>(w.pm)[at], w.pl[at]);
+    }
+    for (int off = 1; off < 32; off <<= 1) {
+      const double ol = __shfl_xor_sync(kFull, ll, off);
+      if constexpr (BWD) {
+        ll += ol;
+      } else {
+        const T om = __shfl_xor_sync(kFull, mm, off);
+        sm_merge<T>(mm, ll, om, ol);
+      }
+    }
+    if (lane != 0) continue;
+    const int64_t row = a.order[r];
+    T* st = static_cast<T*>(a.stat) + row * 2 * (int64_t)a.H + c;
+    if constexpr (BWD) {
+      const T hi = (T)ll;
+      st[0] = hi;
+      st[a.H] = (T)(ll - (double)hi);
+    } else {
+      st[0] = mm;
+      st[a.H] = (T)(1.0 / ll);
     }
   }
 }
@@ -344,7 +508,7 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
             r[k] = (T)__fmaf_rn((float)x[u][k], dh, __fmul_rn((float)x[u][k], dc));
           }
         } else {
-          r[k] = exp_t(T(x[u][k] - p0[u][k])) * p1[u][k];
+          r[k] = softmax_exp(x[u][k], p0[u][k]) * p1[u][k];
         }
       }
       store_vec<T, V>(static_cast<T*>(a.out) + ev[u] * a.ldo + cv[u], r);
@@ -354,6 +518,8 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
 
 cudaError_t launch_edge_softmax(int dtype_is_f64, int V, bool bwd, bool uv, const SoftmaxArgs& a,
                                 int64_t grid, cudaStream_t s);
+cudaError_t launch_edge_softmax_window(int dtype_is_f64, int V, bool bwd, const SoftmaxArgs& a,
+                                       const WindowArgs& w, cudaStream_t s);
 cudaError_t launch_edge_softmax_apply(int dtype_is_f64, int V, bool bwd, bool uv,
                                       const SoftmaxArgs& a, cudaStream_t s);
 

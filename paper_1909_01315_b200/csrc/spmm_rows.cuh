@@ -126,8 +126,16 @@ __device__ __forceinline__ void attn_row_consts(const SpmmArgs& a, int64_t row, 
   }
 }
 
-__device__ __forceinline__ float attn_exp(float x) { return expf(x); }
-__device__ __forceinline__ double attn_exp(double x) { return exp(x); }
+// exp(x - m) of an attention weight: the same formula as softmax.cuh's
+// softmax_exp (2^((x - m) log2 e) on the SFU for fp32), so a recomputed
+// weight equals the one the normalisation kernel would store, bit for bit
+constexpr float kAttnLog2e = 1.4426950408889634f;
+__device__ __forceinline__ float attn_exp(float x, float m) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmaf_rn(x, kAttnLog2e, -m * kAttnLog2e)));
+  return y;
+}
+__device__ __forceinline__ double attn_exp(double x, double m) { return exp(x - m); }
 
 // attention weight of the edge to/from neighbour nb; same fp operation
 // order as the fused softmax (softmax.cuh: s = el + er; exp(s - max) * inv).
@@ -138,12 +146,12 @@ __device__ __forceinline__ T attn_alpha(const SpmmArgs& a, uint32_t nb, const T 
   if constexpr (MP == MP_AF) {
     w = T(0);
     const T x = __ldg(static_cast<const T*>(a.attn_el) + (uint64_t)nb * a.attn_lde) + rc[0];
-    return attn_exp(T(x - rc[1])) * rc[2];
+    return attn_exp(x, rc[1]) * rc[2];
   } else {
     T er, mx, inv;
     load_pack4<T>(static_cast<const T*>(a.attn_pack) + (uint64_t)nb * 4, er, mx, inv, w);
     const T x = rc[0] + er;
-    return attn_exp(T(x - mx)) * inv;
+    return attn_exp(x, mx) * inv;
   }
 }
 

@@ -614,11 +614,37 @@ def extrema_backward_copy(g, aux, dZ, target, rows):
 # fused edge_softmax (replaces the 4-dispatch composition of messaging.py:105-126)
 
 
+def _sorted_eids(adj):
+    """The adjacency's edge ids with each row's ids ascending (cached): the
+    edge ids themselves when they already ascend inside every row (CSC rows
+    sorted by (source, edge id) over an edge list grouped by source), else a
+    per-row sorted copy. Enables the windowed softmax statistics."""
+    se = adj._extra.get("sorted_eids")
+    if se is None:
+        e = adj.edge_ids
+        m, n = e.numel(), adj.num_groups
+        se = e
+        if m > 1:
+            deg = adj.degrees()
+            start = torch.zeros(m, dtype=torch.bool, device=e.device)
+            start[adj.indptr[:-1][deg > 0]] = True
+            if bool(((e[1:] < e[:-1]) & ~start[1:]).any()):
+                row = torch.repeat_interleave(torch.arange(n, device=e.device), deg)
+                key = row * m + e.to(torch.int64)
+                se = e.index_select(0, torch.sort(key).indices)
+        adj._extra["sorted_eids"] = se
+    return se
+
+
 def _softmax_call(g, fn_name, S, G2, H, out, what):
     lib = _lib.load()
     adj = g.to_csc()
     sched = adj.schedule()
-    ws_bytes = int(lib.gmp_edge_softmax_workspace_size(g.num_nodes, H))
+    if sched.n_heavy and g.num_edges >= (1 << 22) and not sched.struct.sorted_eids:
+        sched.struct.sorted_eids = _sorted_eids(adj).data_ptr()
+    ws_bytes = int(lib.gmp_edge_softmax_workspace_size_ex(
+        ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), H, _dtype_code(S),
+        1 if G2 is not None else 0))
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=g.device)
     coo = _lib.GmpCoo(g.num_nodes, g.num_edges, g.src.data_ptr(), g.dst.data_ptr())
     args = [ctypes.byref(_adj_struct(adj)), ctypes.byref(coo), ctypes.byref(sched.struct),
