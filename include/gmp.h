@@ -238,6 +238,7 @@ int gmp_gather_rows(int64_t n, int32_t dim, int dtype, const int32_t* idx, const
                     int64_t lds, void* dst, int64_t ldd, void* stream);
 
 /* ---- column-tile packing ----------------------------------------------------
+ * tile: a power of two >= 2.
  * packed (ceil(d/tile), n, tile): packed[t][r][c] = src[r][t*tile + c], zero
  * past column d. A g-SpMM over a wide src operand then runs one launch per
  * column tile on packed[t] (ld = tile): each per-edge gather is an aligned

@@ -268,31 +268,47 @@ cudaError_t launch_gather_rows(int f64, int64_t n, int32_t dim, const int32_t* i
 // row becomes one aligned tw-element run, so the row kernel's per-edge gather
 // of a tile is whole 32 B sectors with 128-bit loads whatever the caller's ld.
 
+// grid.y = tile; x = (row, column pair) with shifts only (power-of-two tile
+// width); adjacent threads touch adjacent columns, so loads and stores are
+// coalesced on both sides.
 template <typename T>
-__global__ void pack_tiles_kernel(int64_t n, int32_t d, int32_t tw, int32_t ntiles,
-                                  const T* __restrict__ src, int64_t lds, T* __restrict__ dst) {
-  const int64_t total = (int64_t)ntiles * n * tw;
+__global__ void pack_tiles_kernel(int64_t n, int32_t d, int32_t tw, const T* __restrict__ src,
+                                  int64_t lds, T* __restrict__ dst) {
+  const int t = blockIdx.y;
+  const int half = tw >> 1;  // column pairs per tile row (a power of two)
+  const int hl = __ffs(half) - 1;
+  const int64_t total = n * half;
+  const int c_base = t * tw;
+  T* out = dst + (int64_t)t * n * tw;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % tw);
-    const int64_t tr = i / tw;
-    const int64_t r = tr % n;
-    const int t = (int)(tr / n);
-    const int col = t * tw + c;
-    dst[i] = col < d ? src[r * lds + col] : T(0);
+    const int64_t r = i >> hl;
+    const int c = (int)(i & (half - 1)) * 2;
+    const int col = c_base + c;
+    const T* sp = src + r * lds + col;
+    const T v0 = col < d ? sp[0] : T(0);
+    const T v1 = col + 1 < d ? sp[1] : T(0);
+    out[r * tw + c] = v0;
+    out[r * tw + c + 1] = v1;
   }
 }
 
 template <typename T>
 __global__ void unpack_tiles_kernel(int64_t n, int32_t d, int32_t tw, const T* __restrict__ src,
                                     T* __restrict__ dst, int64_t ldd) {
-  const int64_t total = n * (int64_t)d;
+  const int t = blockIdx.y;
+  const int half = tw >> 1;
+  const int hl = __ffs(half) - 1;
+  const int64_t total = n * half;
+  const int c_base = t * tw;
+  const T* in = src + (int64_t)t * n * tw;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / d;
-    const int col = (int)(i - r * d);
-    const int t = col / tw;
-    dst[r * ldd + col] = src[((int64_t)t * n + r) * tw + (col - t * tw)];
+    const int64_t r = i >> hl;
+    const int c = (int)(i & (half - 1)) * 2;
+    const int col = c_base + c;
+    if (col < d) dst[r * ldd + col] = in[r * tw + c];
+    if (col + 1 < d) dst[r * ldd + col + 1] = in[r * tw + c + 1];
   }
 }
 
@@ -300,14 +316,16 @@ cudaError_t launch_pack_tiles(int f64, bool unpack, int64_t n, int32_t d, int32_
                               const void* src, int64_t lds, void* dst, int64_t ldd,
                               cudaStream_t s) {
   const int32_t ntiles = (d + tw - 1) / tw;
-  const int64_t total = unpack ? n * (int64_t)d : (int64_t)ntiles * n * tw;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 32));
+  if (tw < 2 || (tw & (tw - 1))) return cudaErrorInvalidValue;  // a power-of-two tile
+  const int64_t total = n * (int64_t)(tw / 2);
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 4)),
+                  (unsigned)ntiles);
   if (f64) {
     if (unpack) unpack_tiles_kernel<double><<<grid, 256, 0, s>>>(n, d, tw, (const double*)src, (double*)dst, ldd);
-    else pack_tiles_kernel<double><<<grid, 256, 0, s>>>(n, d, tw, ntiles, (const double*)src, lds, (double*)dst);
+    else pack_tiles_kernel<double><<<grid, 256, 0, s>>>(n, d, tw, (const double*)src, lds, (double*)dst);
   } else {
     if (unpack) unpack_tiles_kernel<float><<<grid, 256, 0, s>>>(n, d, tw, (const float*)src, (float*)dst, ldd);
-    else pack_tiles_kernel<float><<<grid, 256, 0, s>>>(n, d, tw, ntiles, (const float*)src, lds, (float*)dst);
+    else pack_tiles_kernel<float><<<grid, 256, 0, s>>>(n, d, tw, (const float*)src, lds, (float*)dst);
   }
   return cudaGetLastError();
 }
