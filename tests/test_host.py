@@ -196,3 +196,80 @@ def test_rmat_cpu_shape_and_range():
     assert s.numel() == 5000 and int(s.max()) < 1000 and int(d.max()) < 1000
     s2, _ = G.generators.rmat_edges(1000, 5000, seed=1, device="cpu")
     assert torch.equal(s, s2)
+
+
+# ---- round-1 additions: tiled path selection, window eid order, new APIs --
+
+def test_tiled_path_selection():
+    from paper_1909_01315_b200.kernels import _tiled_applies
+    n = 232965
+    X = torch.empty((n, 602))
+    W = torch.empty((10, 1))
+    cp = kernels.copy("src")
+    assert _tiled_applies(cp, "sum", X, None, 602, n, None)
+    assert _tiled_applies(cp, "mean", X, None, 602, n, None)
+    assert not _tiled_applies(cp, "max", X, None, 602, n, None)      # arg output: untiled
+    assert not _tiled_applies(cp, "sum", X[:, :64], None, 64, n, None)  # one tile
+    assert not _tiled_applies(cp, "sum", torch.empty((n, 640)), None, 640, n, None)  # aligned
+    assert not _tiled_applies(cp, "sum", X, None, 602, n, (62, 0))     # user tile override
+    assert not _tiled_applies(cp, "sum", torch.empty((100, 602)), None, 602, 100, None)  # fits L2
+    mul = kernels.mul("src", "edge")
+    assert _tiled_applies(mul, "sum", X, W, 602, n, None)
+    assert not _tiled_applies(mul, "sum", X, torch.empty((10, 602)), 602, n, None)
+    assert not _tiled_applies(kernels.mul("dst", "edge"), "sum", X, W, 602, n, None)
+
+
+def test_host_pipeline_tile_bounds():
+    from paper_1909_01315_b200.pipeline import tile_bounds
+    tiles, w = tile_bounds(602, 4)
+    assert w == 64 and len(tiles) == 10
+    assert tiles[0] == (0, 64) and tiles[-1] == (576, 602)
+    tiles, w = tile_bounds(602, 8)
+    assert w == 32 and tiles[-1] == (576, 602)
+
+
+def test_sorted_eids_per_row_on_cpu():
+    """_sorted_eids: the edge ids themselves when they ascend inside every
+    CSC row, else a per-row sorted copy (torch ops only)."""
+    g = cpu_graph(4, [(0, 1), (2, 1), (1, 0), (3, 1)])
+    adj = g.to_csc()
+    assert kernels._sorted_eids(adj) is adj.edge_ids
+    # row 1 in CSC order: src 0 (e2), src 2 (e0), src 3 (e1) -> eids 2, 0, 1
+    g2 = cpu_graph(4, [(2, 1), (3, 1), (0, 1), (1, 0)])
+    a2 = g2.to_csc()
+    se = kernels._sorted_eids(a2)
+    assert se is not a2.edge_ids
+    ip = to_np(a2.indptr)
+    for r in range(4):
+        seg = to_np(se)[ip[r]:ip[r + 1]]
+        assert list(seg) == sorted(to_np(a2.edge_ids)[ip[r]:ip[r + 1]])
+
+
+def test_new_entry_points_refuse_cpu_graph():
+    g = cpu_graph(3, [(0, 2), (1, 2), (2, 0)])
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        G.neighbor_sample(g, [2], fanout=1, rng_seed=0)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        G.update_all_udf(g, lambda c: c.src_rows, lambda b: b.sum(dim=1),
+                         src_feat=np.ones((3, 1)))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        kernels.edge_softmax_uv_stats(g, torch.zeros((3, 1)), torch.zeros((3, 1)))
+
+
+def test_neighbor_sample_validates_before_device():
+    g = cpu_graph(3, [(0, 2), (1, 2), (2, 0)])
+    with pytest.raises(ValueError, match="fanout"):
+        G.neighbor_sample(g, [0], fanout=0, rng_seed=0)
+    with pytest.raises(IndexError):
+        G.neighbor_sample(g, [7], fanout=2, rng_seed=0)
+
+
+def test_layer_order_validation():
+    from paper_1909_01315_b200 import layers
+    W = torch.zeros((602, 16))
+    assert layers._project_first(None, W, "auto")
+    assert not layers._project_first(None, torch.zeros((16, 41)), "auto")
+    assert layers._project_first(None, torch.zeros((16, 41)), "project_first")
+    assert not layers._project_first(None, W, "aggregate_first")
+    with pytest.raises(ValueError):
+        layers._project_first(None, W, "sideways")
