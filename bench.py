@@ -358,12 +358,23 @@ def main():
                          "edges, d=%d, %d threads" % (r, e, F, workers)}
 
     traffic = None
+    l2 = None
     tpath = ROOT / "profiles" / "ncu_traffic.json"
     if tpath.exists():
         try:
             tj = json.loads(tpath.read_text())
             if tj.get("feat") == F and tj.get("edges") == m:
                 traffic = tj.get("dram_bytes_per_launch")
+                l2b = tj.get("row_kernel_l2_read_bytes")
+                cpath = ROOT / "profiles" / "l2_gather_ceiling.json"
+                if l2b and cpath.exists():
+                    ceil = float(json.loads(cpath.read_text())["ceiling_gbs_60mb"])
+                    ach = l2b / (ms * 1e-3) / 1e9
+                    l2 = {"read_bytes_per_step": l2b, "achieved_gbs": round(ach, 1),
+                          "gather_ceiling_gbs": ceil, "frac": round(ach / ceil, 4),
+                          "source": "profiles/ncu_traffic.json (ncu L2 sectors of the row "
+                                    "kernel launches) over this run's step time; ceiling "
+                                    "profiles/l2_gather_ceiling.json"}
         except Exception:
             traffic = None
 
@@ -386,8 +397,14 @@ def main():
                        "graph_gen_s": round(gen_s, 1), "csc_build_s": round(build_s, 2)},
             "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(value / peak, 4), "traffic": traffic,
-                         "peak_kind": peak_kind, "kernel": "spmm_rows_kernel<float,COPY,SUM>",
-                         "bytes_per_launch": step_bytes},
+                         "peak_kind": peak_kind,
+                         "kernel": "spmm_rows_kernel<float,COPY,SUM> over packed 256 B column tiles",
+                         "bytes_per_launch": step_bytes,
+                         "note": "achieved = algorithmic (no-reuse) bytes per step / step time; "
+                                 "frac > 1 because each column tile of X is L2-resident while "
+                                 "every row gathers it - traffic is the measured DRAM bytes and "
+                                 "l2 the bound that binds",
+                         "l2": l2},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),
