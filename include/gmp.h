@@ -230,6 +230,21 @@ int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* ar
                          const void* dZ, int64_t lddz, const int32_t* target_index,
                          void* dOut, int64_t ldo, void* stream);
 
+/* Fused max/min backward for binary messages (add / sub / mul / div): the
+ * gradient of the lhs (role 0) or rhs (role 1) operand, straight from the
+ * winning edges arg (n_rows, d), without route_extrema_grad's (m, d) matrix
+ * (kernels.py:843-857 + autodiff.py:289-372). Cell (v, k) with winner e adds
+ * dZ[v,k] * dphi/doperand (fp64, the reference's expression order; 0 where a
+ * divisor is 0) to the operand's row src[e] / v / e. own_dim: 1 for a
+ * broadcast operand (its cells sum) else d. out (zero-filled by the caller,
+ * rows of the operand's target, ldo). Source rows and broadcast operands
+ * accumulate with atomics (tolerance-level order); destination and edge
+ * rows of full-width operands are written once (bit-exact). */
+int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dtype,
+                           const int64_t* arg, const void* dZ, int64_t lddz, int op, int role,
+                           const gmp_operand* lhs, const gmp_operand* rhs, void* out, int64_t ldo,
+                           int32_t own_dim, void* stream);
+
 /* ---- row gather ------------------------------------------------------------
  * dst[i, :] = src[idx[i], :] for i < n (dim columns). Used to lay an edge
  * operand out in adjacency order once (idx = the adjacency's eids) so that a

@@ -162,11 +162,29 @@ def gspmm_backward(g, phi, rho, X=None, Y=None, W=None, Z=None, aux=None, dZ=Non
         fused = _fused_extrema_copy(g, phi, aux, dZ, needs)
         if fused is not None:
             return fused
+        if phi.op in ("add", "sub", "mul", "div"):
+            return _fused_extrema_binary(g, phi, aux, dZ, X, Y, W, needs)
         up = kernels.route_extrema_grad(g, aux, dZ, dZ.shape[1])
         up_slot = "edge"
     else:
         raise ValueError("unknown reducer %r" % (rho,))
     return _edge_grads(g, phi, X, Y, W, up, up_slot, needs)
+
+
+def _fused_extrema_binary(g, phi, aux, dZ, X, Y, W, needs):
+    """add / sub / mul / div under max/min: one kernel per needed operand
+    gradient straight from the winning edges (gmp_extrema_bwd_binary)."""
+    slot = {"src": "x", "dst": "y", "edge": "w"}
+    attr = {"src": "dx", "dst": "dy", "edge": "dw"}
+    bundle = GradBundle()
+    for role, t in ((0, phi.lhs_target), (1, phi.rhs_target)):
+        if slot[t] not in needs:
+            continue
+        accounting.log_dispatch("gsddmm", g.uid, "argext_grad(%s,%d)" % (phi.describe(), role),
+                                "-", "edge_parallel", g.num_edges, dZ.shape[1])
+        res = kernels.extrema_backward_binary(g, aux, dZ, phi, role, X, Y, W)
+        setattr(bundle, attr[t], res)
+    return bundle
 
 
 def _fused_extrema_copy(g, phi, aux, dZ, needs):

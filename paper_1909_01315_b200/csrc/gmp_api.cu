@@ -26,6 +26,20 @@ cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const
 size_t schedule_workspace_bytes(int64_t n);
 cudaError_t launch_gather_rows(int, int64_t, int32_t, const int32_t*, const void*, int64_t, void*,
                                int64_t, cudaStream_t);
+struct ExtBinArgs {
+  int64_t n;
+  int32_t d;
+  const int64_t* arg;
+  const void* dZ;
+  int64_t lddz;
+  const int32_t* src;
+  int32_t op, role, target;
+  OperandDev lhs, rhs;
+  void* out;
+  int64_t ldo;
+  int32_t own_dim;
+};
+cudaError_t launch_extrema_bwd_binary(int, const ExtBinArgs&, cudaStream_t);
 cudaError_t launch_pack_tiles(int, bool, int64_t, int32_t, int32_t, const void*, int64_t, void*,
                               int64_t, cudaStream_t);
 cudaError_t launch_neighbor_sample(const int64_t*, const int64_t*, int64_t, const int64_t*, uint64_t,
@@ -699,6 +713,35 @@ int gmp_unpack_tiles(int64_t n, int32_t d, int dtype, int32_t tile, const void* 
                                     (cudaStream_t)stream);
   g_launches++;
   return cuda_status(e, "gmp_unpack_tiles");
+}
+
+int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dtype,
+                           const int64_t* arg, const void* dZ, int64_t lddz, int op, int role,
+                           const gmp_operand* lhs, const gmp_operand* rhs, void* out, int64_t ldo,
+                           int32_t own_dim, void* stream) {
+  if (!coo || !lhs || !rhs) return fail(GMP_EINVAL, "null coo / operand");
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (op != GMP_ADD && op != GMP_SUB && op != GMP_MUL && op != GMP_DIV)
+    return fail(GMP_EINVAL, "binary extrema backward takes add / sub / mul / div, got %s",
+                op_name(op));
+  if (role != 0 && role != 1) return fail(GMP_EINVAL, "role must be 0 (lhs) or 1 (rhs)");
+  if (n_rows < 0 || d < 0 || lddz < d || (own_dim != 1 && own_dim != d) || ldo < own_dim)
+    return fail(GMP_EINVAL, "bad sizes");
+  const gmp_operand* own = role == 0 ? lhs : rhs;
+  if (own->target < GMP_SRC || own->target > GMP_EDGE || lhs->target < GMP_SRC ||
+      lhs->target > GMP_EDGE || rhs->target < GMP_SRC || rhs->target > GMP_EDGE)
+    return fail(GMP_EINVAL, "operand targets must be src / dst / edge");
+  if (n_rows == 0 || d == 0) return GMP_OK;
+  if (!arg || !dZ || !out || !coo->src || !lhs->data || !rhs->data)
+    return fail(GMP_EINVAL, "null arrays");
+  ExtBinArgs a{};
+  a.n = n_rows; a.d = d; a.arg = arg; a.dZ = dZ; a.lddz = lddz; a.src = coo->src;
+  a.op = kernel_op(op); a.role = role; a.target = own->target;
+  a.lhs = to_dev(lhs, d).dev; a.rhs = to_dev(rhs, d).dev;
+  a.out = out; a.ldo = ldo; a.own_dim = own_dim;
+  cudaError_t e = launch_extrema_bwd_binary(dtype == GMP_F64, a, (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_extrema_bwd_binary");
 }
 
 int gmp_neighbor_sample(const int64_t* indptr, int64_t n_rows, const int64_t* seeds,

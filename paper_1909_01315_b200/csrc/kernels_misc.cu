@@ -240,6 +240,75 @@ cudaError_t launch_extrema_bwd_copy(int f64, int64_t n, int32_t d, const int64_t
   return cudaGetLastError();
 }
 
+// Fused max/min backward of a binary message (add / sub / mul / div of two
+// operands): the gradient of one operand straight from the winning edges,
+// without route_extrema_grad's dense (m, d) matrix (kernels.py:843-857 then
+// autodiff.py:289-372). Cell (v, k) with winner e = arg[v, k] contributes
+// dZ[v, k] * d phi / d operand, evaluated in fp64 on the winner's operands
+// (the reference's fp64 expression order), to the operand's row: src[e]
+// (several cells can hit one source row: atomicAdd), v or e (one cell per
+// (row, column): plain store, bit-exact) - a broadcast operand (own_dim == 1)
+// sums its cells with atomicAdd.
+struct ExtBinArgs {
+  int64_t n;
+  int32_t d;
+  const int64_t* arg;
+  const void* dZ;
+  int64_t lddz;
+  const int32_t* src;
+  int32_t op, role, target;
+  OperandDev lhs, rhs;
+  void* out;
+  int64_t ldo;
+  int32_t own_dim;
+};
+
+__device__ __forceinline__ int64_t ext_row(int32_t t, int64_t u, int64_t v, int64_t e) {
+  return t == T_SRC ? u : (t == T_DST ? v : e);
+}
+
+template <typename T>
+__global__ void extrema_bwd_binary_kernel(const ExtBinArgs a) {
+  const int64_t total = a.n * (int64_t)a.d;
+  T* out = static_cast<T*>(a.out);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / a.d;
+    const int k = (int)(i - v * a.d);
+    const int64_t e = a.arg[i];
+    if (e < 0) continue;
+    const int64_t u = __ldg(a.src + e);
+    const double dz = (double)static_cast<const T*>(a.dZ)[v * a.lddz + k];
+    const double av = (double)static_cast<const T*>(a.lhs.data)[
+        ext_row(a.lhs.target, u, v, e) * a.lhs.ld + (a.lhs.dim == 1 ? 0 : k)];
+    const double bv = (double)static_cast<const T*>(a.rhs.data)[
+        ext_row(a.rhs.target, u, v, e) * a.rhs.ld + (a.rhs.dim == 1 ? 0 : k)];
+    double g;
+    switch (a.op) {
+      case OP_ADD: g = dz; break;
+      case OP_SUB: g = a.role == 0 ? dz : -dz; break;
+      case OP_MUL: g = dz * (a.role == 0 ? bv : av); break;
+      default:  // OP_DIV: d(a/b)/da = 1/b, d(a/b)/db = -a/b^2 (0 where b == 0)
+        if (bv == 0.0) g = 0.0;
+        else g = a.role == 0 ? dz / bv : -((dz * av) / (bv * bv));
+        break;
+    }
+    const int64_t row = ext_row(a.target, u, v, e);
+    T* dst = out + row * a.ldo + (a.own_dim == 1 ? 0 : k);
+    if (a.target == T_SRC || a.own_dim == 1) atomicAdd(dst, (T)g);
+    else *dst = (T)g;
+  }
+}
+
+cudaError_t launch_extrema_bwd_binary(int f64, const ExtBinArgs& a, cudaStream_t s) {
+  const int64_t total = a.n * (int64_t)a.d;
+  if (total == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  if (f64) extrema_bwd_binary_kernel<double><<<grid, 256, 0, s>>>(a);
+  else extrema_bwd_binary_kernel<float><<<grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 // ---- row gather: dst[i] = src[idx[i]] ------------------------------------------
 
 template <typename T>

@@ -610,6 +610,33 @@ def extrema_backward_copy(g, aux, dZ, target, rows):
     return out
 
 
+def extrema_backward_binary(g, aux, dZ, phi, role, X, Y, W):
+    """Fused max/min backward of a binary message: the gradient of phi's lhs
+    (role 0) or rhs (role 1) operand from the winning edges, no (m, d)
+    buffer (gmp_extrema_bwd_binary)."""
+    _require_cuda(g)
+    arg = aux.arg_edge.contiguous()
+    dZ = _to_tensor("dZ", dZ, g.device)
+    n, d = arg.shape
+    mats = {"src": X, "dst": Y, "edge": W}
+    own_t = phi.lhs_target if role == 0 else phi.rhs_target
+    own = mats[own_t]
+    rows = g.num_edges if own_t == "edge" else g.num_nodes
+    own_dim = own.shape[1]
+    out = accounting.register(torch.zeros((rows, own_dim), dtype=dZ.dtype, device=g.device))
+    if out.numel() and n and d and g.num_edges:  # no edges: no winners, zero gradient
+        lhs = _lib.GmpOperand(_data_ptr(mats[phi.lhs_target]), _ld(mats[phi.lhs_target]),
+                              mats[phi.lhs_target].shape[1], _lib.TARGETS[phi.lhs_target])
+        rhs = _lib.GmpOperand(_data_ptr(mats[phi.rhs_target]), _ld(mats[phi.rhs_target]),
+                              mats[phi.rhs_target].shape[1], _lib.TARGETS[phi.rhs_target])
+        coo = _lib.GmpCoo(g.num_nodes, g.num_edges, g.src.data_ptr(), g.dst.data_ptr())
+        _lib.check(_lib.load().gmp_extrema_bwd_binary(
+            ctypes.byref(coo), n, d, _dtype_code(dZ), arg.data_ptr(), dZ.data_ptr(), _ld(dZ),
+            _lib.OPS[phi.op], role, ctypes.byref(lhs), ctypes.byref(rhs), out.data_ptr(),
+            own_dim, own_dim, _stream(g.device)), "gmp_extrema_bwd_binary")
+    return out
+
+
 # ----------------------------------------------------------------------------
 # fused edge_softmax (replaces the 4-dispatch composition of messaging.py:105-126)
 
