@@ -754,7 +754,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, GMP_ROW_MIN_BLOCKS)
 spmm_rows_kernel(const SpmmArgs a) {
   using Acc = RowAcc<T, OP, RHO, V>;
   using ExtT = typename Acc::ExtT;
-  constexpr int U = Unroll<V>::value;
+  // run-time operand modes and max/min of binary messages carry more live
+  // state per gather (fp64 messages, both operands, arg): 4 gathers in
+  // flight per lane keeps them in registers (op sweep: div 1.3-2.4x, binary
+  // max/min 1.1-1.4x faster than with 8, which spilled); the narrow / wide
+  // launch split still follows Unroll<V>
+  constexpr int U = (MP == MP_GEN || (RHO != RHO_SUM && OP != OP_COPY)) ? 4 : Unroll<V>::value;
   constexpr int kCols = 32 * V;  // widest tile one warp covers
   __shared__ double s_acc[RHO == RHO_SUM ? kWarpsPerCta : 1][kCols];
   __shared__ ExtT s_cur[RHO == RHO_SUM ? 1 : kWarpsPerCta][kCols];
