@@ -820,7 +820,31 @@ spmm_rows_kernel(const SpmmArgs a) {
 
   Acc acc;
   acc.init();
-  if constexpr (NARROW) {
+  // copy of the destination's own row (copy_lhs(dst) / copy_rhs(dst)): every
+  // message of the row is Y[v], so sum = deg * Y[v] - exact in fp64 for
+  // deg < 2^29, equal to the reference's fp64 accumulation - and no edge
+  // needs to be read (one writer per row: slot 0, warp 0 of a heavy CTA)
+  bool row_const = false;
+  if constexpr (OP == OP_COPY && RHO == RHO_SUM && MP == MP_GEN) {
+    if (a.lhs.mode == M_HOIST) {
+      row_const = true;
+      const bool own = NARROW && light ? true : (slot == 0 && (!heavy || warp == 0));
+      if (own && deg > 0) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc.acc[k] = (double)deg * (double)ha[k];
+      }
+    }
+  }
+  if (row_const) {
+    if constexpr (NARROW) {
+      if (light) {
+        if (row < 0) return;
+        if (a.counts && tile == 0 && gl == 0) a.counts[row] = deg;
+        write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
+        return;
+      }
+    }
+  } else if constexpr (NARROW) {
     if (light) {
       spmm_accumulate_slot<T, OP, RHO, V, MP, U>(a, pb, pe, col, valid, ha, hb, rc, acc);
       if (row < 0) return;
@@ -835,6 +859,8 @@ spmm_rows_kernel(const SpmmArgs a) {
         a, pb, pe, heavy ? (int64_t)warp * kChunkE : 0,
         heavy ? (int64_t)kChunkE * kWarpsPerCta : kChunkE, lane, slot, E, col, valid, ha, hb, rc,
         s_chunk + warp * kChunkE, s_chunk + (kWarpsPerCta + warp) * kChunkE, acc);
+  } else if (row_const) {
+    // nothing to accumulate
   } else if (heavy) {
     spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, (int64_t)warp * 32, 32 * kWarpsPerCta, lane,
                                           slot, E, col, valid, ha, hb, rc, acc);
