@@ -342,12 +342,21 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
     a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.dim = dim;
     const int V = dim > 0 ? pick_v(F, dim, ops, 2, nullptr, 0, nullptr) : 1;
     a.g_log2 = log2i(std::min(32, next_pow2(std::max(1, (dim + V - 1) / V))));
-    a.mean = rho == GMP_MEAN; a.lhs = ops[0].dev; a.rhs = ops[1].dev;
-    a.lhs.bcast = a.rhs.bcast = 0;
-    a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts;
-    e = launch_spmm_dot(F == 8, krho, V, a, bpt, s);
-    g_launches++;
-    return cuda_status(e, "gmp_gspmm(dot)");
+    {
+      // short rows: one per lane group when a row uses fewer than 32 lanes
+      const int Ed = 32 >> a.g_log2;
+      const int64_t n_med = (order && Ed > 1) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
+      a.n_medium = n_med;
+      a.medium_blocks = (n_med - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
+      const int64_t per = (int64_t)kWarpsPerCta * Ed;
+      const int64_t bpt_dot = n_heavy + a.medium_blocks + (adj->n_rows - n_med + per - 1) / per;
+      a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts;
+      a.mean = rho == GMP_MEAN; a.lhs = ops[0].dev; a.rhs = ops[1].dev;
+      a.lhs.bcast = a.rhs.bcast = 0;
+      e = launch_spmm_dot(F == 8, krho, V, a, bpt_dot, s);
+      g_launches++;
+      return cuda_status(e, "gmp_gspmm(dot)");
+    }
   }
 
   const int V = pick_v(F, d_out, ops, 2, Z, ldz, ext ? arg : nullptr);

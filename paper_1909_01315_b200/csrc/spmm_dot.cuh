@@ -19,6 +19,8 @@ struct SpmmDotArgs {
   const int32_t* order;
   int64_t n_rows;
   int64_t n_heavy;
+  int64_t n_medium;       // rows [n_heavy, n_medium): one warp each; the rest one per lane group
+  int64_t medium_blocks;  // CTAs covering the warp rows
   int32_t dim;     // operand width
   int32_t g_log2;  // lanes per edge
   int32_t mean;
@@ -57,36 +59,87 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) spmm_dot_kernel(const SpmmD
   const int G = 1 << a.g_log2, E = 32 >> a.g_log2;
   const int slot = lane >> a.g_log2, gl = lane & (G - 1);
   const bool heavy = local < a.n_heavy;
+  const bool light = local >= a.n_heavy + a.medium_blocks;  // block-uniform
   int64_t row;
   if (heavy) {
     row = a.order[local];
-  } else {
+  } else if (!light) {
     const int64_t r = a.n_heavy + (local - a.n_heavy) * kWarpsPerCta + warp;
-    if (r >= a.n_rows) return;
+    if (r >= a.n_medium) return;
     row = a.order ? (int64_t)a.order[r] : r;
+  } else {
+    // short rows (<= light threshold in-edges): each lane group owns a row
+    // and walks its edges itself, E rows per warp
+    const int64_t r = a.n_medium +
+                      ((local - a.n_heavy - a.medium_blocks) * kWarpsPerCta + warp) * E + slot;
+    if (__all_sync(kFull, r >= a.n_rows)) return;
+    row = r < a.n_rows ? (a.order ? (int64_t)a.order[r] : r) : -1;
   }
-  const int64_t pb = a.indptr[row], pe = a.indptr[row + 1], deg = pe - pb;
+  const int64_t pb = row >= 0 ? a.indptr[row] : 0, pe = row >= 0 ? a.indptr[row + 1] : 0;
+  const int64_t deg = pe - pb;
   double acc = (RHO == RHO_SUM) ? 0.0 : ext_init<RHO>();
   int32_t arg = 0x7fffffff;
-  const int64_t first = heavy ? (int64_t)warp * 32 : 0;
-  const int64_t stride = heavy ? 32 * kWarpsPerCta : 32;
-  for (int64_t base = pb + first; base < pe; base += stride) {
-    const int cnt = batch_count(pe - base);
-    int nb = 0, eb = 0;
-    if (lane < cnt) {
-      nb = __ldg(a.indices + base + lane);
-      eb = __ldg(a.eids + base + lane);
-    }
-    for (int t = 0; t < cnt; t += E) {
-      const int j = t + slot;
-      const int32_t uu = __shfl_sync(kFull, nb, j & 31);
-      const int32_t ee = __shfl_sync(kFull, eb, j & 31);
+  if (light) {
+    const int max_deg = (int)__reduce_max_sync(kFull, (unsigned)deg);
+    for (int j = 0; j < max_deg; ++j) {
+      const bool ok = j < deg;
+      const int32_t uu = ok ? __ldg(a.indices + pb + j) : 0;
+      const int32_t ee = ok ? __ldg(a.eids + pb + j) : 0;
       double s = 0.0;
-      if (j < cnt) s = dot_partial<T, V>(a.lhs, a.rhs, row, uu, ee, gl, G, a.dim);
+      if (ok) s = dot_partial<T, V>(a.lhs, a.rhs, row, uu, ee, gl, G, a.dim);
       for (int off = 1; off < G; off <<= 1) s += shfl_xor_d(s, off);
-      if (j < cnt) {
+      if (ok) {
         if constexpr (RHO == RHO_SUM) acc += s;
         else ext_update<RHO>(acc, arg, s, ee);
+      }
+    }
+    if (row < 0 || gl != 0) return;
+    T* z = static_cast<T*>(a.Z) + row * a.ldz;
+    if (a.counts) a.counts[row] = deg;
+    if constexpr (RHO == RHO_SUM) {
+      double v = acc;
+      if (a.mean && deg > 0) v = v / (double)deg;
+      *z = (T)v;
+    } else {
+      *z = deg > 0 ? (T)acc : T(0);
+      a.arg[row] = deg > 0 ? arg : -1;
+    }
+    return;
+  }
+  const int64_t first = heavy ? (int64_t)warp * 32 : 0;
+  const int64_t stride = heavy ? 32 * kWarpsPerCta : 32;
+  // kDotU batches per iteration: their index loads and dot products are
+  // independent, so a lane keeps kDotU edges in flight (hub rows would
+  // otherwise walk one dependent load chain per 32 edges)
+  constexpr int kDotU = 4;
+  for (int64_t base0 = pb + first; base0 < pe; base0 += stride * kDotU) {
+    int nb[kDotU], eb[kDotU], cnt[kDotU];
+#pragma unroll
+    for (int u = 0; u < kDotU; ++u) {
+      const int64_t base = base0 + u * stride;
+      cnt[u] = base < pe ? batch_count(pe - base) : 0;
+      nb[u] = lane < cnt[u] ? __ldg(a.indices + base + lane) : 0;
+      eb[u] = lane < cnt[u] ? __ldg(a.eids + base + lane) : 0;
+    }
+    for (int t = 0; t < 32; t += E) {
+      double sv[kDotU];
+      int32_t ev[kDotU];
+#pragma unroll
+      for (int u = 0; u < kDotU; ++u) {
+        const int j = t + slot;
+        const int32_t uu = __shfl_sync(kFull, nb[u], j & 31);
+        ev[u] = __shfl_sync(kFull, eb[u], j & 31);
+        sv[u] = 0.0;
+        if (j < cnt[u]) sv[u] = dot_partial<T, V>(a.lhs, a.rhs, row, uu, ev[u], gl, G, a.dim);
+      }
+#pragma unroll
+      for (int u = 0; u < kDotU; ++u) {
+        double s = sv[u];
+        for (int off = 1; off < G; off <<= 1) s += shfl_xor_d(s, off);
+        if (t + slot < cnt[u]) {
+          if constexpr (RHO == RHO_SUM) acc += s;
+          else ext_update<RHO>(acc, arg, s, ev[u]);
+        }
       }
     }
   }
