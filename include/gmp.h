@@ -66,7 +66,9 @@ typedef struct {
  * sorted_eids (nullable): the adjacency's edge ids with each row's ids in
  * ascending order (equal to eids when they already ascend inside rows); when
  * given, edge-keyed passes over heavy rows (edge_softmax statistics) run in
- * L2-sized edge-id windows. */
+ * L2-sized edge-id windows. When the largest row holds more than half of one
+ * SM's share of the edges, heavy rows are reduced by a cluster of 8 CTAs
+ * (partials merged through distributed shared memory, in rank order). */
 typedef struct {
   const int32_t* order;
   int64_t n_heavy;
@@ -75,6 +77,7 @@ typedef struct {
   int32_t heavy_threshold;
   int32_t light_threshold;
   const int32_t* sorted_eids;
+  int64_t max_degree;      /* largest row degree (set by gmp_build_schedule) */
 } gmp_sched;
 
 /* COO edge list in edge-id order (graph.py:98-100). */

@@ -37,7 +37,7 @@ class GmpSched(ctypes.Structure):
     _fields_ = [("order", ctypes.c_void_p), ("n_heavy", ctypes.c_int64),
                 ("n_medium", ctypes.c_int64), ("n_nonempty", ctypes.c_int64),
                 ("heavy_threshold", ctypes.c_int32), ("light_threshold", ctypes.c_int32),
-                ("sorted_eids", ctypes.c_void_p)]
+                ("sorted_eids", ctypes.c_void_p), ("max_degree", ctypes.c_int64)]
 
 
 class GmpCoo(ctypes.Structure):

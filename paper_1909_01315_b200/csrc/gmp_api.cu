@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/gmp.h"
@@ -47,7 +48,8 @@ cudaError_t launch_neighbor_sample(const int64_t*, const int64_t*, int64_t, cons
 int softmax_window_resident_ctas(int f64, int V, bool bwd);
 cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t light,
                            int32_t* order_out, void* ws, size_t ws_bytes, int64_t* n_heavy,
-                           int64_t* n_medium, int64_t* n_nonempty, cudaStream_t s);
+                           int64_t* n_medium, int64_t* n_nonempty, int64_t* max_degree,
+                           cudaStream_t s);
 }  // namespace gmp
 
 using namespace gmp;
@@ -114,6 +116,26 @@ Opnd to_dev(const gmp_operand* o, int d_out) {
   r.dev.bcast = (o->dim == 1 && d_out > 1) ? 1 : 0;
   return r;
 }
+
+// CTAs per heavy row: a thread-block cluster of 8 when the largest row alone
+// holds more than half of one SM's share of the edges (otherwise that row's
+// single CTA is the kernel's tail) and an edge carries enough work (width >=
+// 4 columns; below that the extra CTAs cost more than the tail, op sweep);
+// GMP_NO_CLUSTER=1 disables it.
+int hub_cluster(const gmp_adj* adj, const gmp_sched* sched, int width) {
+  static const bool off = getenv("GMP_NO_CLUSTER") != nullptr;
+  if (off || !sched || sched->n_heavy <= 0 || adj->m <= 0 || width < 4) return 1;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sched->max_degree * 2 * (int64_t)sms > adj->m ? 8 : 1;
+}
+
+int64_t round_up(int64_t x, int64_t k) { return (x + k - 1) / k * k; }
 
 // Largest vector width every full-width operand, the output and arg support.
 int pick_v(size_t F, int width, const Opnd* ops, int nops, const void* out, int64_t ldo,
@@ -250,9 +272,9 @@ int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold, int32_t ligh
                 schedule_workspace_bytes(adj->n_rows));
   if (light_threshold < 0 || light_threshold > heavy_threshold)
     return fail(GMP_EINVAL, "light threshold must be in [0, heavy threshold]");
-  int64_t nh = 0, nm = 0, nn = 0;
+  int64_t nh = 0, nm = 0, nn = 0, dmax = 0;
   cudaError_t e = build_schedule(adj->n_rows, adj->indptr, heavy_threshold, light_threshold,
-                                 order_out, workspace, workspace_bytes, &nh, &nm, &nn,
+                                 order_out, workspace, workspace_bytes, &nh, &nm, &nn, &dmax,
                                  (cudaStream_t)stream);
   g_launches += adj->n_rows > 0 ? 2 : 0;
   if (e != cudaSuccess) return cuda_status(e, "gmp_build_schedule");
@@ -262,6 +284,7 @@ int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold, int32_t ligh
   sched_out->n_nonempty = nn;
   sched_out->heavy_threshold = heavy_threshold;
   sched_out->light_threshold = light_threshold;
+  sched_out->max_degree = dmax;
   return GMP_OK;
 }
 
@@ -320,8 +343,11 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
       a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
       a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_med;
       a.medium_blocks = med_blocks;
-      a.blocks_per_tile = n_heavy + med_blocks +
-                          (adj->n_rows - n_med + rows_per_light_cta - 1) / rows_per_light_cta;
+      a.cluster = hub_cluster(adj, sched, dim);
+      a.blocks_per_tile = round_up(
+          n_heavy * a.cluster + med_blocks +
+              (adj->n_rows - n_med + rows_per_light_cta - 1) / rows_per_light_cta,
+          a.cluster);
       a.d_out = dim; a.tile_cols = dim; a.g_log2 = log2i(Gd); a.mean = rho == GMP_MEAN;
       a.lhs = row_operand(ops[0]);
       a.rhs = row_operand(ops[1]);
@@ -374,9 +400,15 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
   const int64_t n_medium = (order && narrow) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
   const int64_t medium_blocks = (n_medium - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
   const int64_t light_rows = adj->n_rows - n_medium;
-  const int64_t bpt_rows = n_heavy + medium_blocks +
-                           (light_rows + (int64_t)kWarpsPerCta * E - 1) / ((int64_t)kWarpsPerCta * E);
+  // a copy of the destination's own row reads no edges (row-constant path)
+  const bool row_const = kop == OP_COPY && ops[0].dev.target == GMP_DST;
+  const int ncl = hub_cluster(adj, sched, row_const ? 0 : tw);
+  const int64_t bpt_rows = round_up(
+      n_heavy * ncl + medium_blocks +
+          (light_rows + (int64_t)kWarpsPerCta * E - 1) / ((int64_t)kWarpsPerCta * E),
+      ncl);
   SpmmArgs a{};
+  a.cluster = ncl;
   a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
   a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_medium;
   a.medium_blocks = medium_blocks; a.blocks_per_tile = bpt_rows;
@@ -680,9 +712,13 @@ int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int
   const int64_t n_medium = (order && narrow) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
   const int64_t medium_blocks = (n_medium - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
   const int64_t light_rows = adj->n_rows - n_medium;
-  const int64_t bpt_rows = n_heavy + medium_blocks +
-                           (light_rows + (int64_t)kWarpsPerCta * E - 1) / ((int64_t)kWarpsPerCta * E);
+  const int ncl = hub_cluster(adj, sched, tw);
+  const int64_t bpt_rows = round_up(
+      n_heavy * ncl + medium_blocks +
+          (light_rows + (int64_t)kWarpsPerCta * E - 1) / ((int64_t)kWarpsPerCta * E),
+      ncl);
   SpmmArgs a{};
+  a.cluster = ncl;
   a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
   a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_medium;
   a.medium_blocks = medium_blocks; a.blocks_per_tile = bpt_rows;

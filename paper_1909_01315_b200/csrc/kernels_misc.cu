@@ -404,7 +404,7 @@ cudaError_t launch_pack_tiles(int f64, bool unpack, int64_t n, int32_t d, int32_
 __global__ void degree_kernel(int64_t n, const int64_t* __restrict__ indptr, int32_t* deg,
                               int32_t* rows, int32_t thr, int32_t light,
                               unsigned long long* counters) {
-  unsigned long long heavy = 0, nonempty = 0, medium = 0;
+  unsigned long long heavy = 0, nonempty = 0, medium = 0, dmax = 0;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t dg = indptr[r + 1] - indptr[r];
@@ -413,16 +413,20 @@ __global__ void degree_kernel(int64_t n, const int64_t* __restrict__ indptr, int
     heavy += dg > thr;
     nonempty += dg > 0;
     medium += dg > light;
+    dmax = dmax > (unsigned long long)dg ? dmax : (unsigned long long)dg;
   }
   for (int off = 16; off > 0; off >>= 1) {
     heavy += __shfl_xor_sync(kFull, heavy, off);
     nonempty += __shfl_xor_sync(kFull, nonempty, off);
     medium += __shfl_xor_sync(kFull, medium, off);
+    const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
+    dmax = dmax > o ? dmax : o;
   }
   if ((threadIdx.x & 31) == 0) {
     if (heavy) atomicAdd(counters, heavy);
     if (nonempty) atomicAdd(counters + 1, nonempty);
     if (medium) atomicAdd(counters + 2, medium);
+    if (dmax) atomicMax(counters + 3, dmax);
   }
 }
 
@@ -442,7 +446,8 @@ size_t schedule_workspace_bytes(int64_t n) {
 
 cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t light,
                            int32_t* order_out, void* ws, size_t ws_bytes, int64_t* n_heavy,
-                           int64_t* n_medium, int64_t* n_nonempty, cudaStream_t s) {
+                           int64_t* n_medium, int64_t* n_nonempty, int64_t* max_degree,
+                           cudaStream_t s) {
   char* p = static_cast<char*>(ws);
   auto* counters = reinterpret_cast<unsigned long long*>(p);
   p += align256(32);
@@ -462,13 +467,14 @@ cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_
                                                     (int)n, 0, 32, s);
     if (err != cudaSuccess) return err;
   }
-  unsigned long long host[3] = {0, 0, 0};
-  err = cudaMemcpyAsync(host, counters, 24, cudaMemcpyDeviceToHost, s);
+  unsigned long long host[4] = {0, 0, 0, 0};
+  err = cudaMemcpyAsync(host, counters, 32, cudaMemcpyDeviceToHost, s);
   if (err != cudaSuccess) return err;
   err = cudaStreamSynchronize(s);
   *n_heavy = (int64_t)host[0];
   *n_nonempty = (int64_t)host[1];
   *n_medium = (int64_t)host[2];
+  *max_degree = (int64_t)host[3];
   return err;
 }
 

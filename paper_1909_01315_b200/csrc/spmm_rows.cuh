@@ -37,6 +37,8 @@
 
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "gmp_common.cuh"
 
 namespace gmp {
@@ -98,6 +100,7 @@ struct SpmmArgs {
   uint32_t attn_lde;
   const void* attn_pack;  // (n, 4) rows [er, max, inv_sum, w]
   double* attn_t;         // MP_AB: t[u] = sum_{u->v} alpha_e w[v] (nullable)
+  int32_t cluster;        // CTAs per heavy row (a thread-block cluster), 1 = one CTA
 };
 
 template <typename T>
@@ -777,19 +780,23 @@ spmm_rows_kernel(const SpmmArgs a) {
   const int E = 32 >> a.g_log2;
   const int slot = lane >> a.g_log2;
   const int gl = lane & (G - 1);
-  const bool heavy = local < a.n_heavy;  // block-uniform
-  const bool light = NARROW && local >= a.n_heavy + a.medium_blocks;  // block-uniform
+  // heavy rows: `cl` CTAs each (one thread-block cluster, rank crank)
+  const int ncl = a.cluster > 1 ? a.cluster : 1;
+  const int64_t heavy_blocks = a.n_heavy * ncl;
+  const bool heavy = local < heavy_blocks;  // block-uniform
+  const int crank = heavy ? (int)(local % ncl) : 0;
+  const bool light = NARROW && local >= heavy_blocks + a.medium_blocks;  // block-uniform
 
   int64_t row;
   if (heavy) {
-    row = a.order[local];
+    row = a.order[local / ncl];
   } else if (!light) {
-    const int64_t r = a.n_heavy + (local - a.n_heavy) * kWarpsPerCta + warp;
+    const int64_t r = a.n_heavy + (local - heavy_blocks) * kWarpsPerCta + warp;
     if (r >= a.n_medium) return;  // warp rows never synchronise the CTA
     row = a.order ? (int64_t)a.order[r] : r;
   } else {
     const int64_t r = a.n_medium +
-                      ((local - a.n_heavy - a.medium_blocks) * kWarpsPerCta + warp) * E + slot;
+                      ((local - heavy_blocks - a.medium_blocks) * kWarpsPerCta + warp) * E + slot;
     if (__all_sync(kFull, r >= a.n_rows)) return;
     row = r < a.n_rows ? (a.order ? (int64_t)a.order[r] : r) : -1;  // -1: idle slot
   }
@@ -828,7 +835,8 @@ spmm_rows_kernel(const SpmmArgs a) {
   if constexpr (OP == OP_COPY && RHO == RHO_SUM && MP == MP_GEN) {
     if (a.lhs.mode == M_HOIST) {
       row_const = true;
-      const bool own = NARROW && light ? true : (slot == 0 && (!heavy || warp == 0));
+      const bool own = NARROW && light ? true
+                                       : (slot == 0 && (!heavy || (warp == 0 && crank == 0)));
       if (own && deg > 0) {
 #pragma unroll
         for (int k = 0; k < V; ++k) acc.acc[k] = (double)deg * (double)ha[k];
@@ -856,14 +864,15 @@ spmm_rows_kernel(const SpmmArgs a) {
       return;
     }
     spmm_accumulate_chunked<T, OP, RHO, V, MP, U>(
-        a, pb, pe, heavy ? (int64_t)warp * kChunkE : 0,
-        heavy ? (int64_t)kChunkE * kWarpsPerCta : kChunkE, lane, slot, E, col, valid, ha, hb, rc,
+        a, pb, pe, heavy ? ((int64_t)crank * kWarpsPerCta + warp) * kChunkE : 0,
+        heavy ? (int64_t)kChunkE * kWarpsPerCta * ncl : kChunkE, lane, slot, E, col, valid, ha, hb, rc,
         s_chunk + warp * kChunkE, s_chunk + (kWarpsPerCta + warp) * kChunkE, acc);
   } else if (row_const) {
     // nothing to accumulate
   } else if (heavy) {
-    spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, (int64_t)warp * 32, 32 * kWarpsPerCta, lane,
-                                          slot, E, col, valid, ha, hb, rc, acc);
+    spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, ((int64_t)crank * kWarpsPerCta + warp) * 32,
+                                          (int64_t)32 * kWarpsPerCta * ncl, lane, slot, E, col,
+                                          valid, ha, hb, rc, acc);
   } else {
     spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, 0, 32, lane, slot, E, col, valid, ha, hb,
                                           rc, acc);
@@ -873,7 +882,7 @@ spmm_rows_kernel(const SpmmArgs a) {
     for (int off = 16; off > 0; off >>= 1) acc.tsum += __shfl_xor_sync(kFull, acc.tsum, off);
   }
 
-  if (a.counts && tile == 0 && ((heavy && threadIdx.x == 0) || (!heavy && lane == 0)))
+  if (a.counts && tile == 0 && ((heavy && crank == 0 && threadIdx.x == 0) || (!heavy && lane == 0)))
     a.counts[row] = deg;
 
   if (!heavy) {
@@ -915,14 +924,64 @@ spmm_rows_kernel(const SpmmArgs a) {
         for (int w = 1; w < kWarpsPerCta; ++w) acc.merge(k, 0.0, s_cur[w][cl], s_arg[w][cl]);
       }
     }
-    write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
+    double t = 0.0;
     if constexpr (MP == MP_AB) {
-      if (a.attn_t && tile == 0 && lane == 0) {
-        double t = s_t[0];
+      if (lane == 0) {
+        t = s_t[0];
         for (int w = 1; w < kWarpsPerCta; ++w) t += s_t[w];
-        a.attn_t[row] = t;
       }
     }
+    if (ncl == 1) {
+      write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
+      if constexpr (MP == MP_AB) {
+        if (a.attn_t && tile == 0 && lane == 0) a.attn_t[row] = t;
+      }
+    } else {
+      // this CTA's partial of the row, for the cluster merge below
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int cl = gl * V + k;
+        if constexpr (RHO == RHO_SUM) {
+          s_acc[0][cl] = acc.acc[k];
+        } else {
+          s_cur[0][cl] = acc.cur[k];
+          s_arg[0][cl] = acc.arg[k];
+        }
+      }
+      if constexpr (MP == MP_AB) {
+        if (lane == 0) s_t[0] = t;
+      }
+    }
+  }
+  if (ncl > 1) {
+    // the row's CTAs form one cluster: rank 0 reads the other ranks'
+    // partials from their shared memory (DSMEM) and merges them in rank order
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (crank == 0 && warp == 0 && slot == 0) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int cl = gl * V + k;
+        for (int r = 1; r < ncl; ++r) {
+          if constexpr (RHO == RHO_SUM) {
+            acc.acc[k] += *cluster.map_shared_rank(&s_acc[0][cl], r);
+          } else {
+            acc.merge(k, 0.0, *cluster.map_shared_rank(&s_cur[0][cl], r),
+                      *cluster.map_shared_rank(&s_arg[0][cl], r));
+          }
+        }
+      }
+      write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
+      if constexpr (MP == MP_AB) {
+        if (a.attn_t && tile == 0 && lane == 0) {
+          double t = s_t[0];
+          for (int r = 1; r < ncl; ++r) t += *cluster.map_shared_rank(&s_t[0], r);
+          a.attn_t[row] = t;
+        }
+      }
+    }
+    cluster.sync();  // the partials stay readable until rank 0 is done
   }
 }
 
@@ -931,17 +990,38 @@ __host__ __device__ constexpr bool narrow_launch(int g_log2) {
   return (32 >> g_log2) > 1 && (32 >> g_log2) * Unroll<V>::value > 32;
 }
 
+// a.cluster > 1: launched as thread-block clusters of a.cluster CTAs (grid a
+// multiple of it) so a heavy row's CTAs can merge through DSMEM
+template <typename Kern>
+cudaError_t launch_rows_cfg(Kern kern, const SpmmArgs& a, int64_t grid, size_t smem,
+                            cudaStream_t s) {
+  if (a.cluster <= 1) {
+    kern<<<(unsigned)grid, kWarpsPerCta * 32, smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.blockDim = dim3(kWarpsPerCta * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)a.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 template <typename T, int OP, int RHO, int V, int MP>
 cudaError_t launch_spmm_rows_t(const SpmmArgs& a, int64_t grid, cudaStream_t s) {
   if constexpr (sizeof(T) == 4) {
-    if (narrow_launch<V>(a.g_log2)) {
-      spmm_rows_kernel<T, OP, RHO, V, MP, true>
-          <<<(unsigned)grid, kWarpsPerCta * 32, 2 * kWarpsPerCta * kChunkE * sizeof(int32_t), s>>>(a);
-      return cudaGetLastError();
-    }
+    if (narrow_launch<V>(a.g_log2))
+      return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, true>, a, grid,
+                             2 * kWarpsPerCta * kChunkE * sizeof(int32_t), s);
   }
-  spmm_rows_kernel<T, OP, RHO, V, MP, false><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false>, a, grid, 0, s);
 }
 
 // float: hot mode pairs get their own kernels; double (the parity
