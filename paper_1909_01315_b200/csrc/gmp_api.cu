@@ -367,7 +367,9 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
     a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
     a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.dim = dim;
     const int V = dim > 0 ? pick_v(F, dim, ops, 2, nullptr, 0, nullptr) : 1;
-    a.g_log2 = log2i(std::min(32, next_pow2(std::max(1, (dim + V - 1) / V))));
+    // at most 8 lanes per edge: wide dots loop over columns instead of
+    // paying a 5-level fp64 shuffle tree per edge
+    a.g_log2 = log2i(std::min(8, next_pow2(std::max(1, (dim + V - 1) / V))));
     {
       // short rows: one per lane group when a row uses fewer than 32 lanes
       const int Ed = 32 >> a.g_log2;
@@ -375,7 +377,10 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
       a.n_medium = n_med;
       a.medium_blocks = (n_med - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
       const int64_t per = (int64_t)kWarpsPerCta * Ed;
-      const int64_t bpt_dot = n_heavy + a.medium_blocks + (adj->n_rows - n_med + per - 1) / per;
+      a.cluster = hub_cluster(adj, sched, dim);
+      const int64_t bpt_dot = round_up(
+          n_heavy * a.cluster + a.medium_blocks + (adj->n_rows - n_med + per - 1) / per,
+          a.cluster);
       a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts;
       a.mean = rho == GMP_MEAN; a.lhs = ops[0].dev; a.rhs = ops[1].dev;
       a.lhs.bcast = a.rhs.bcast = 0;

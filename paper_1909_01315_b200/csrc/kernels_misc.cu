@@ -8,9 +8,30 @@
 
 namespace gmp {
 
+// a.cluster > 1: thread-block clusters of a.cluster CTAs (heavy-row merge via DSMEM)
+template <typename Kern>
+static void launch_dot_cfg(Kern kern, const SpmmDotArgs& a, int64_t grid, cudaStream_t s) {
+  if (a.cluster <= 1) {
+    kern<<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.blockDim = dim3(kWarpsPerCta * 32, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)a.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 cudaError_t launch_spmm_dot(int f64, int rho, int V, const SpmmDotArgs& a, int64_t grid,
                             cudaStream_t s) {
-#define GMP_DOT(T, R, VV) spmm_dot_kernel<T, R, VV><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a)
+#define GMP_DOT(T, R, VV) launch_dot_cfg(spmm_dot_kernel<T, R, VV>, a, grid, s)
 #define GMP_DOT_V(T, R)            \
   do {                             \
     if (V == 4 && sizeof(T) == 4)  \

@@ -29,6 +29,7 @@ struct SpmmDotArgs {
   int64_t ldz;
   int64_t* arg;
   int64_t* counts;
+  int32_t cluster;  // CTAs per heavy row (thread-block cluster), 1 = one CTA
 };
 
 template <typename T, int V>
@@ -58,20 +59,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) spmm_dot_kernel(const SpmmD
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = 1 << a.g_log2, E = 32 >> a.g_log2;
   const int slot = lane >> a.g_log2, gl = lane & (G - 1);
-  const bool heavy = local < a.n_heavy;
-  const bool light = local >= a.n_heavy + a.medium_blocks;  // block-uniform
+  const int ncl = a.cluster > 1 ? a.cluster : 1;
+  const int64_t heavy_blocks = a.n_heavy * ncl;
+  const bool heavy = local < heavy_blocks;
+  const int crank = heavy ? (int)(local % ncl) : 0;
+  const bool light = local >= heavy_blocks + a.medium_blocks;  // block-uniform
   int64_t row;
   if (heavy) {
-    row = a.order[local];
+    row = a.order[local / ncl];
   } else if (!light) {
-    const int64_t r = a.n_heavy + (local - a.n_heavy) * kWarpsPerCta + warp;
+    const int64_t r = a.n_heavy + (local - heavy_blocks) * kWarpsPerCta + warp;
     if (r >= a.n_medium) return;
     row = a.order ? (int64_t)a.order[r] : r;
   } else {
     // short rows (<= light threshold in-edges): each lane group owns a row
     // and walks its edges itself, E rows per warp
     const int64_t r = a.n_medium +
-                      ((local - a.n_heavy - a.medium_blocks) * kWarpsPerCta + warp) * E + slot;
+                      ((local - heavy_blocks - a.medium_blocks) * kWarpsPerCta + warp) * E + slot;
     if (__all_sync(kFull, r >= a.n_rows)) return;
     row = r < a.n_rows ? (a.order ? (int64_t)a.order[r] : r) : -1;
   }
@@ -106,8 +110,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) spmm_dot_kernel(const SpmmD
     }
     return;
   }
-  const int64_t first = heavy ? (int64_t)warp * 32 : 0;
-  const int64_t stride = heavy ? 32 * kWarpsPerCta : 32;
+  const int64_t first = heavy ? ((int64_t)crank * kWarpsPerCta + warp) * 32 : 0;
+  const int64_t stride = heavy ? (int64_t)32 * kWarpsPerCta * ncl : 32;
   // kDotU batches per iteration: their index loads and dot products are
   // independent, so a lane keeps kDotU edges in flight (hub rows would
   // otherwise walk one dependent load chain per 32 edges)
@@ -151,12 +155,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) spmm_dot_kernel(const SpmmD
   if (heavy) {
     if (lane == 0) { s_acc[warp] = acc; s_arg[warp] = arg; }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    acc = s_acc[0]; arg = s_arg[0];
-    for (int w = 1; w < kWarpsPerCta; ++w) {
-      if constexpr (RHO == RHO_SUM) acc += s_acc[w];
-      else ext_update<RHO>(acc, arg, s_acc[w], s_arg[w]);
+    if (threadIdx.x == 0) {
+      acc = s_acc[0]; arg = s_arg[0];
+      for (int w = 1; w < kWarpsPerCta; ++w) {
+        if constexpr (RHO == RHO_SUM) acc += s_acc[w];
+        else ext_update<RHO>(acc, arg, s_acc[w], s_arg[w]);
+      }
     }
+    if (ncl > 1) {
+      // the row's CTAs form a cluster: rank 0 merges the ranks' partials
+      // from their shared memory (DSMEM) in rank order
+      namespace cg = cooperative_groups;
+      cg::cluster_group cluster = cg::this_cluster();
+      if (threadIdx.x == 0) { s_acc[0] = acc; s_arg[0] = arg; }
+      cluster.sync();
+      if (threadIdx.x == 0 && crank == 0) {
+        for (int r = 1; r < ncl; ++r) {
+          const double o = *cluster.map_shared_rank(&s_acc[0], r);
+          const int32_t oa = *cluster.map_shared_rank(&s_arg[0], r);
+          if constexpr (RHO == RHO_SUM) acc += o;
+          else ext_update<RHO>(acc, arg, o, oa);
+        }
+      }
+      cluster.sync();
+      if (crank != 0) return;
+    }
+    if (threadIdx.x != 0) return;
   } else if (lane != 0) {
     return;
   }

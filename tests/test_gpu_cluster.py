@@ -73,3 +73,20 @@ def test_cluster_gat_attention_matches_composition():
     alpha = kernels.edge_softmax_uv_forward(g, el, er)
     comp, _ = G.gspmm(g, kernels.mul("src", "edge"), "sum", X=X, W=alpha)
     assert torch.equal(fused, comp)
+
+
+@pytest.mark.parametrize("rho", ["sum", "max", "min"])
+def test_cluster_dot_rows_match_oracle(rho):
+    s, d, n = hub_graph()
+    g = G.from_arrays(s, d, num_nodes=n, device=DEV)
+    rng = np.random.default_rng(3)
+    x = rng.integers(-2, 3, (n, 8)).astype(np.float32)  # small ints: exact dots, many ties
+    X = torch.as_tensor(x, device=DEV)
+    z, aux = G.gspmm(g, kernels.dot("src", "dst"), rho, X=X, Y=X)
+    want, waux = O.gspmm(s, d, n, "dot", "src", "dst", rho, X=x.astype(np.float64),
+                         Y=x.astype(np.float64))
+    if rho == "sum":
+        assert np.allclose(to_np(z), want, rtol=RTOL32, atol=ATOL32)
+    else:
+        assert np.array_equal(to_np(z), want.astype(np.float32))
+        assert np.array_equal(to_np(aux.arg_edge), waux)
