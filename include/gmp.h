@@ -233,7 +233,7 @@ int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* ar
                          const void* dZ, int64_t lddz, const int32_t* target_index,
                          void* dOut, int64_t ldo, void* stream);
 
-/* Fused max/min backward for binary messages (add / sub / mul / div): the
+/* Fused max/min backward for binary messages (add / sub / mul / div / dot): the
  * gradient of the lhs (role 0) or rhs (role 1) operand, straight from the
  * winning edges arg (n_rows, d), without route_extrema_grad's (m, d) matrix
  * (kernels.py:843-857 + autodiff.py:289-372). Cell (v, k) with winner e adds
@@ -242,7 +242,8 @@ int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* ar
  * broadcast operand (its cells sum) else d. out (zero-filled by the caller,
  * rows of the operand's target, ldo). Source rows and broadcast operands
  * accumulate with atomics (tolerance-level order); destination and edge
- * rows of full-width operands are written once (bit-exact). */
+ * rows of full-width operands are written once (bit-exact). dot: d == 1 and
+ * own_dim is the operand width (the gradient row is dZ[v] * the other row). */
 int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dtype,
                            const int64_t* arg, const void* dZ, int64_t lddz, int op, int role,
                            const gmp_operand* lhs, const gmp_operand* rhs, void* out, int64_t ldo,

@@ -162,7 +162,7 @@ def gspmm_backward(g, phi, rho, X=None, Y=None, W=None, Z=None, aux=None, dZ=Non
         fused = _fused_extrema_copy(g, phi, aux, dZ, needs)
         if fused is not None:
             return fused
-        if phi.op in ("add", "sub", "mul", "div"):
+        if phi.op in ("add", "sub", "mul", "div", "dot"):
             return _fused_extrema_binary(g, phi, aux, dZ, X, Y, W, needs)
         up = kernels.route_extrema_grad(g, aux, dZ, dZ.shape[1])
         up_slot = "edge"

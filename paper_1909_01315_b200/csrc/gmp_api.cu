@@ -771,11 +771,14 @@ int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dt
                            int32_t own_dim, void* stream) {
   if (!coo || !lhs || !rhs) return fail(GMP_EINVAL, "null coo / operand");
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
-  if (op != GMP_ADD && op != GMP_SUB && op != GMP_MUL && op != GMP_DIV)
-    return fail(GMP_EINVAL, "binary extrema backward takes add / sub / mul / div, got %s",
+  if (op != GMP_ADD && op != GMP_SUB && op != GMP_MUL && op != GMP_DIV && op != GMP_DOT)
+    return fail(GMP_EINVAL, "binary extrema backward takes add / sub / mul / div / dot, got %s",
                 op_name(op));
+  if (op == GMP_DOT && (d != 1 || lhs->dim != rhs->dim || own_dim != lhs->dim))
+    return fail(GMP_EINVAL, "dot: d_out must be 1 and own_dim the operand width");
   if (role != 0 && role != 1) return fail(GMP_EINVAL, "role must be 0 (lhs) or 1 (rhs)");
-  if (n_rows < 0 || d < 0 || lddz < d || (own_dim != 1 && own_dim != d) || ldo < own_dim)
+  if (n_rows < 0 || d < 0 || lddz < d || ldo < own_dim ||
+      (op != GMP_DOT && own_dim != 1 && own_dim != d))
     return fail(GMP_EINVAL, "bad sizes");
   const gmp_operand* own = role == 0 ? lhs : rhs;
   if (own->target < GMP_SRC || own->target > GMP_EDGE || lhs->target < GMP_SRC ||
@@ -787,7 +790,8 @@ int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dt
   ExtBinArgs a{};
   a.n = n_rows; a.d = d; a.arg = arg; a.dZ = dZ; a.lddz = lddz; a.src = coo->src;
   a.op = kernel_op(op); a.role = role; a.target = own->target;
-  a.lhs = to_dev(lhs, d).dev; a.rhs = to_dev(rhs, d).dev;
+  a.lhs = to_dev(lhs, op == GMP_DOT ? lhs->dim : d).dev;
+  a.rhs = to_dev(rhs, op == GMP_DOT ? rhs->dim : d).dev;
   a.out = out; a.ldo = ldo; a.own_dim = own_dim;
   cudaError_t e = launch_extrema_bwd_binary(dtype == GMP_F64, a, (cudaStream_t)stream);
   g_launches++;

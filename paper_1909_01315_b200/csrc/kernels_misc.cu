@@ -288,6 +288,29 @@ __device__ __forceinline__ int64_t ext_row(int32_t t, int64_t u, int64_t v, int6
   return t == T_SRC ? u : (t == T_DST ? v : e);
 }
 
+// dot messages (d_out == 1): cell (v, c) for every operand column c adds
+// dZ[v] * other[c] to the operand's row (d(a.b)/da = b)
+template <typename T>
+__global__ void extrema_bwd_dot_kernel(const ExtBinArgs a) {
+  const int64_t total = a.n * (int64_t)a.own_dim;
+  T* out = static_cast<T*>(a.out);
+  const OperandDev& other = a.role == 0 ? a.rhs : a.lhs;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / a.own_dim;
+    const int c = (int)(i - v * a.own_dim);
+    const int64_t e = a.arg[v];
+    if (e < 0) continue;
+    const int64_t u = __ldg(a.src + e);
+    const double dz = (double)static_cast<const T*>(a.dZ)[v * a.lddz];
+    const double ov = (double)static_cast<const T*>(other.data)[
+        ext_row(other.target, u, v, e) * other.ld + c];
+    T* dst = out + ext_row(a.target, u, v, e) * a.ldo + c;
+    if (a.target == T_SRC) atomicAdd(dst, (T)(dz * ov));
+    else *dst = (T)(dz * ov);
+  }
+}
+
 template <typename T>
 __global__ void extrema_bwd_binary_kernel(const ExtBinArgs a) {
   const int64_t total = a.n * (int64_t)a.d;
@@ -322,6 +345,14 @@ __global__ void extrema_bwd_binary_kernel(const ExtBinArgs a) {
 }
 
 cudaError_t launch_extrema_bwd_binary(int f64, const ExtBinArgs& a, cudaStream_t s) {
+  if (a.op == OP_DOT) {
+    const int64_t total = a.n * (int64_t)a.own_dim;
+    if (total == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    if (f64) extrema_bwd_dot_kernel<double><<<grid, 256, 0, s>>>(a);
+    else extrema_bwd_dot_kernel<float><<<grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   const int64_t total = a.n * (int64_t)a.d;
   if (total == 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);

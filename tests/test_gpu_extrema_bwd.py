@@ -19,10 +19,12 @@ PAIRS = [("src", "dst"), ("dst", "src"), ("src", "edge"), ("edge", "src"), ("dst
          ("edge", "dst")]
 
 
-@pytest.mark.parametrize("op", ["add", "sub", "mul", "div"])
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "div", "dot"])
 @pytest.mark.parametrize("rho", ["max", "min"])
 @pytest.mark.parametrize("bcast", [False, True])
 def test_fused_binary_extrema_backward_matches_composition(op, rho, bcast):
+    if op == "dot" and bcast:
+        pytest.skip("dot needs equal operand widths (kernels.py:242-246)")
     s, d = G.generators.power_law_edges(4000, 10, seed=5)
     n, m = 4000, s.size
     g = G.from_arrays(s, d, num_nodes=n, device=DEV)
