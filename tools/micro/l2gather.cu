@@ -16,20 +16,20 @@ __global__ void gen_idx(uint32_t* idx, int64_t n, uint32_t rows) {
   }
 }
 
-template <int U>
+template <int U, int L = 16>
 __global__ void __launch_bounds__(256) gather(const float4* __restrict__ data,
                                               const uint32_t* __restrict__ idx, int64_t n,
                                               float* out) {
-  const int lane = threadIdx.x & 15;  // 16 lanes per 256 B row
-  const int64_t groups = (int64_t)gridDim.x * blockDim.x / 16;
+  const int lane = threadIdx.x & (L - 1);  // L lanes x 16 B per row
+  const int64_t groups = (int64_t)gridDim.x * blockDim.x / L;
   float acc = 0.f;
-  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 16; g * U < n; g += groups) {
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / L; g * U < n; g += groups) {
     float4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t e = g * U + u;
       const uint32_t r = e < n ? __ldg(idx + e) : 0;
-      v[u] = __ldg(data + (int64_t)r * 16 + lane);
+      v[u] = __ldg(data + (int64_t)r * L + lane);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
@@ -57,6 +57,19 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, a, b);
     ms /= 5;
     printf("slice %4d MB: %.3f ms  %.1f GB/s of 256 B rows gathered\n", mb, ms, n * 256.0 / ms / 1e6);
+  }
+  // 64 B rows (d = 16 fp32: the GCN hidden layer), X of the Reddit shape (15 MB)
+  for (int mb : {15, 60}) {
+    const uint32_t rows = (uint32_t)(((int64_t)mb << 20) / 64);
+    gen_idx<<<1184, 256>>>(idx, n, rows);
+    gather<8, 4><<<sms * 8, 256>>>(data, idx, n, out);
+    cudaEventRecord(a);
+    for (int rep = 0; rep < 5; ++rep) gather<8, 4><<<sms * 8, 256>>>(data, idx, n, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    ms /= 5;
+    printf("slice %4d MB: %.3f ms  %.1f GB/s of 64 B rows gathered\n", mb, ms, n * 64.0 / ms / 1e6);
   }
   return 0;
 }
