@@ -83,3 +83,39 @@ def test_error_string_is_thread_local():
     t.join()
     assert seen == [b""]
     assert b"unknown op" in lib.gmp_last_error()
+
+
+def test_round1_entry_points_validate_without_gpu():
+    """The entry points added this round reject bad arguments before any
+    CUDA call, with a detail string."""
+    lib = _lib.load()
+    p = ctypes.c_void_p(256)
+    adj = _lib.GmpAdj(3, 3, p, p, p)
+    # gat aggregate: leading dimension smaller than the width
+    st = lib.gmp_gat_aggregate(ctypes.byref(adj), None, 0, 0, p, 2, 4, p, 1, p, p, 4, None, None,
+                               None)
+    assert st == _lib.GMP_EINVAL and b"leading" in lib.gmp_last_error()
+    # uv stats: null el / er
+    st = lib.gmp_edge_softmax_uv_stats(ctypes.byref(adj), None, 0, None, 1, None, 1, 1, p, 64,
+                                       None)
+    assert st == _lib.GMP_EINVAL and b"el / er" in lib.gmp_last_error()
+    # pack: tile must be a power of two is checked by the launcher; bad ld here
+    st = lib.gmp_pack_tiles(10, 8, 0, 64, p, 4, p, None)
+    assert st == _lib.GMP_EINVAL and b"bad sizes" in lib.gmp_last_error()
+    # binary extrema backward: copy is not a binary op
+    coo = _lib.GmpCoo(3, 3, p, p)
+    x = _lib.GmpOperand(p, 4, 4, _lib.TARGETS["src"])
+    w = _lib.GmpOperand(p, 1, 1, _lib.TARGETS["edge"])
+    st = lib.gmp_extrema_bwd_binary(ctypes.byref(coo), 3, 4, 0, p, p, 4, _lib.OPS["copy_lhs"], 0,
+                                    ctypes.byref(x), ctypes.byref(w), p, 4, 4, None)
+    assert st == _lib.GMP_EINVAL and b"binary extrema backward" in lib.gmp_last_error()
+    # dot: d_out must be 1
+    st = lib.gmp_extrema_bwd_binary(ctypes.byref(coo), 3, 4, 0, p, p, 4, _lib.OPS["dot"], 0,
+                                    ctypes.byref(x), ctypes.byref(x), p, 4, 4, None)
+    assert st == _lib.GMP_EINVAL and b"d_out must be 1" in lib.gmp_last_error()
+    # neighbour sample: negative sizes
+    st = lib.gmp_neighbor_sample(p, -1, p, 1, p, 0, p, p, None)
+    assert st == _lib.GMP_EINVAL and b"bad sizes" in lib.gmp_last_error()
+    # windowed softmax workspace: no schedule -> the plain size
+    assert lib.gmp_edge_softmax_workspace_size_ex(ctypes.byref(adj), None, 8, 0, 0) == \
+        lib.gmp_edge_softmax_workspace_size(3, 8)
