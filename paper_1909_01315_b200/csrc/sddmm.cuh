@@ -115,8 +115,14 @@ __global__ void __launch_bounds__(256) sddmm_kernel(const SddmmArgs a) {
 template <typename T, int V>
 __global__ void __launch_bounds__(256) sddmm_dot_lane_kernel(const SddmmArgs a) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.m; e += stride) {
-    const int32_t u = __ldg(a.src + e), v = __ldg(a.dst + e);
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // the next edge's (src, dst) are loaded while the current edge's rows are
+  // gathered and reduced: the DRAM read of the ids leaves the dependent chain
+  int32_t un = 0, vn = 0;
+  if (e < a.m) { un = __ldg(a.src + e); vn = __ldg(a.dst + e); }
+  for (; e < a.m; e += stride) {
+    const int32_t u = un, v = vn;
+    if (e + stride < a.m) { un = __ldg(a.src + e + stride); vn = __ldg(a.dst + e + stride); }
     const T* pa = static_cast<const T*>(a.lhs.data) + operand_row(a.lhs, u, v, e) * a.lhs.ld;
     const T* pb = static_cast<const T*>(a.rhs.data) + operand_row(a.rhs, u, v, e) * a.rhs.ld;
     double r;
