@@ -90,3 +90,29 @@ def test_cluster_dot_rows_match_oracle(rho):
     else:
         assert np.array_equal(to_np(z), want.astype(np.float32))
         assert np.array_equal(to_np(aux.arg_edge), waux)
+
+
+def test_cluster_gat_backward_on_reverse_hub():
+    """A source with 40k out-edges: the reverse-graph row of the fused GAT
+    backward (MP_AB, t = sum alpha * S merged across ranks) runs on a cluster;
+    gradients against the composed path (autograd through edge_softmax_uv
+    and the u_mul_e g-SpMM)."""
+    rng = np.random.default_rng(12)
+    n = 3000
+    s = np.concatenate([np.full(40000, 9), rng.integers(0, n, 20000)])
+    d = np.concatenate([rng.integers(0, n, 40000), rng.integers(0, n, 20000)])
+    g = G.from_arrays(s, d, num_nodes=n, device=DEV)
+    rsched = G.reverse(g).to_csc().schedule()
+    assert rsched.struct.max_degree >= 40000
+    t = [torch.as_tensor(rng.standard_normal(sh), device=DEV).requires_grad_(True)
+         for sh in ((n, 1), (n, 1), (n, 16))]
+    up = torch.as_tensor(rng.standard_normal((n, 16)), device=DEV)
+    (G.autodiff.gat_attention(g, *t) * up).sum().backward()
+    fused = [x.grad.clone() for x in t]
+    for x in t:
+        x.grad = None
+    alpha = G.autodiff.edge_softmax_uv(g, t[0], t[1])
+    z = G.autodiff.gspmm(g, kernels.mul("src", "edge"), "sum", X=t[2], W=alpha)
+    (z * up).sum().backward()
+    for got, x in zip(fused, t):
+        assert torch.allclose(got, x.grad, rtol=1e-9, atol=1e-11)
