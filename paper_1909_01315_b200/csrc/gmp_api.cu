@@ -513,7 +513,11 @@ static WindowPlan window_plan(const gmp_adj* adj, const gmp_sched* sched, int32_
   const int64_t warps = (int64_t)softmax_window_resident_ctas(F == 8, V, bwd) * kWarpsPerCta;
   const int64_t inflight = (warps + R - 1) / R + 1;  // windows touched by the warps in flight
   const int64_t row_bytes = (int64_t)H * (int64_t)F * (bwd ? 2 : 1);
-  const int64_t budget = 80ll << 20;
+  static const int64_t budget_mb = [] {
+    const char* v = getenv("GMP_SOFTMAX_L2_MB");
+    return v ? std::max<int64_t>(8, atoll(v)) : 80;
+  }();
+  const int64_t budget = budget_mb << 20;
   const int64_t win = budget / (inflight * row_bytes);
   if (win < (1 << 15)) return p;
   p.win = win;
