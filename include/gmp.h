@@ -216,6 +216,13 @@ int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int
                       const void* pack, void* Z, int64_t ldz, double* t_out,
                       const gmp_tuning* tuning, void* stream);
 
+/* Node-level epilogue of the fused GAT backward: out[v * out_stride] =
+ * sum_c A[v,c] B[v,c] - sub[v] (fp64 accumulation, sub nullable), e.g.
+ * S_v = dZ[v].Z[v] straight into the pack's 4th column, and
+ * d el[u] = X[u].dX[u] - t[u]. */
+int gmp_rowdot(int64_t n, int32_t d, int dtype, const void* A, int64_t lda, const void* B,
+               int64_t ldb, const double* sub, void* out, int64_t out_stride, void* stream);
+
 /* ---- extrema gradient routing ----------------------------------------------
  * Replaces kernels.route_extrema_grad (kernels.py:843-857): dM[arg[v,k], k] =
  * dZ[v,k] for every cell with arg >= 0. dM (m, d) must be zero-filled by the

@@ -23,7 +23,7 @@ EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "g
             "gmp_edge_softmax_workspace_size", "gmp_edge_softmax_workspace_size_ex", "gmp_edge_softmax_fwd", "gmp_edge_softmax_uv_fwd", "gmp_edge_softmax_bwd", "gmp_route_extrema",
             "gmp_extrema_bwd_copy", "gmp_gather_rows", "gmp_neighbor_sample",
             "gmp_edge_softmax_uv_stats", "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
-            "gmp_extrema_bwd_binary", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
+            "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
             "gmp_version")
 
 
@@ -95,6 +95,7 @@ def _declare(lib):
     lib.gmp_gat_aggregate.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, c_int, vp, i64, i32, vp,
                                       i64, vp, vp, i64, vp, _P(GmpTuning), vp]
     lib.gmp_pack_tiles.argtypes = [i64, i32, c_int, i32, vp, i64, vp, vp]
+    lib.gmp_rowdot.argtypes = [i64, i32, c_int, vp, i64, vp, i64, vp, vp, i64, vp]
     lib.gmp_extrema_bwd_binary.argtypes = [_P(GmpCoo), i64, i32, c_int, vp, vp, i64, c_int, c_int,
                                            _P(GmpOperand), _P(GmpOperand), vp, i64, i32, vp]
     lib.gmp_unpack_tiles.argtypes = [i64, i32, c_int, i32, vp, vp, i64, vp]
@@ -107,7 +108,7 @@ def _declare(lib):
                  "gmp_edge_softmax_bwd", "gmp_route_extrema", "gmp_extrema_bwd_copy",
                  "gmp_gather_rows", "gmp_neighbor_sample", "gmp_edge_softmax_uv_stats",
                  "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
-                 "gmp_extrema_bwd_binary", "gmp_version"):
+                 "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_version"):
         getattr(lib, name).restype = c_int
 
 

@@ -352,17 +352,20 @@ class _GATAttention(torch.autograd.Function):
         g, shared, d = ctx.g, ctx.shared, ctx.d
         H = el.shape[1]
         dout = dout.to(X.dtype)
-        acc = torch.float64
-        dX_parts, del_cols = [], []
+        if dout.stride(-1) != 1:
+            dout = dout.contiguous()
+        dX_parts = []
+        dEl = torch.empty(el.shape, dtype=X.dtype, device=X.device)
         for h in range(H):
             dZh = dout[:, h * d:(h + 1) * d]
             Zh = out[:, h * d:(h + 1) * d]
-            # S_v rides in the pack's 4th column; t[u] = sum_{u->v} alpha_e S_v
+            # S_v = dZ[v].Z[v] (fp64) rides in the pack's 4th column;
+            # t[u] = sum_{u->v} alpha_e S_v comes back from the kernel
             pk = pack[h].clone()
-            pk[:, 3] = (dZh.to(acc) * Zh.to(acc)).sum(1).to(X.dtype)
+            kernels.rowdot(dZh, Zh, pk[:, 3])
             dXh, t = kernels.gat_aggregate(g, dZh, el[:, h:h + 1], pk, backward=True)
             Xh = X if shared else X[:, h * d:(h + 1) * d]
-            del_cols.append(((Xh.to(acc) * dXh.to(acc)).sum(1) - t).to(X.dtype))
+            kernels.rowdot(Xh, dXh, dEl[:, h], sub=t)   # d el = X.dX - t
             dX_parts.append(dXh)
         if shared:
             dX = dX_parts[0]
@@ -370,7 +373,6 @@ class _GATAttention(torch.autograd.Function):
                 dX = dX + p
         else:
             dX = dX_parts[0] if H == 1 else torch.cat(dX_parts, dim=1)
-        dEl = torch.stack(del_cols, dim=1)
         return None, _match(dEl, el), torch.zeros_like(er), _match(dX, X), None
 
 

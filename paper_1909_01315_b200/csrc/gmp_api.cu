@@ -41,6 +41,8 @@ struct ExtBinArgs {
   int32_t own_dim;
 };
 cudaError_t launch_extrema_bwd_binary(int, const ExtBinArgs&, cudaStream_t);
+cudaError_t launch_rowdot(int, int64_t, int32_t, const void*, int64_t, const void*, int64_t,
+                          const double*, void*, int64_t, cudaStream_t);
 cudaError_t launch_pack_tiles(int, bool, int64_t, int32_t, int32_t, const void*, int64_t, void*,
                               int64_t, cudaStream_t);
 cudaError_t launch_neighbor_sample(const int64_t*, const int64_t*, int64_t, const int64_t*, uint64_t,
@@ -800,6 +802,18 @@ int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dt
   cudaError_t e = launch_extrema_bwd_binary(dtype == GMP_F64, a, (cudaStream_t)stream);
   g_launches++;
   return cuda_status(e, "gmp_extrema_bwd_binary");
+}
+
+int gmp_rowdot(int64_t n, int32_t d, int dtype, const void* A, int64_t lda, const void* B,
+               int64_t ldb, const double* sub, void* out, int64_t out_stride, void* stream) {
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (n < 0 || d < 0 || lda < d || ldb < d || out_stride < 1) return fail(GMP_EINVAL, "bad sizes");
+  if (n == 0) return GMP_OK;
+  if ((d > 0 && (!A || !B)) || !out) return fail(GMP_EINVAL, "null arrays");
+  cudaError_t e = launch_rowdot(dtype == GMP_F64, n, d, A, lda, B, ldb, sub, out, out_stride,
+                                (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_rowdot");
 }
 
 int gmp_neighbor_sample(const int64_t* indptr, int64_t n_rows, const int64_t* seeds,

@@ -361,6 +361,34 @@ cudaError_t launch_extrema_bwd_binary(int f64, const ExtBinArgs& a, cudaStream_t
   return cudaGetLastError();
 }
 
+// ---- row dot products: out[v * os] = sum_c A[v,c] B[v,c] - sub[v] (fp64) ---------
+// The fused GAT backward's node-level epilogue (S_v = dZ[v].Z[v] into the
+// pack; d el[u] = X[u].dX[u] - t[u]) in one pass each instead of a chain of
+// elementwise / reduction launches.
+template <typename T>
+__global__ void rowdot_kernel(int64_t n, int32_t d, const T* __restrict__ A, int64_t lda,
+                              const T* __restrict__ B, int64_t ldb,
+                              const double* __restrict__ sub, T* out, int64_t os) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    const T* a = A + v * lda;
+    const T* b = B + v * ldb;
+    for (int c = 0; c < d; ++c) acc += (double)__ldg(a + c) * (double)__ldg(b + c);
+    if (sub) acc -= sub[v];
+    out[v * os] = (T)acc;
+  }
+}
+
+cudaError_t launch_rowdot(int f64, int64_t n, int32_t d, const void* A, int64_t lda, const void* B,
+                          int64_t ldb, const double* sub, void* out, int64_t os, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (f64) rowdot_kernel<double><<<grid, 256, 0, s>>>(n, d, (const double*)A, lda, (const double*)B, ldb, sub, (double*)out, os);
+  else rowdot_kernel<float><<<grid, 256, 0, s>>>(n, d, (const float*)A, lda, (const float*)B, ldb, sub, (float*)out, os);
+  return cudaGetLastError();
+}
+
 // ---- row gather: dst[i] = src[idx[i]] ------------------------------------------
 
 template <typename T>

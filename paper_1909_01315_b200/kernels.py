@@ -610,6 +610,23 @@ def extrema_backward_copy(g, aux, dZ, target, rows):
     return out
 
 
+def rowdot(A, B, out, sub=None):
+    """out[v] = sum_c A[v,c] B[v,c] - sub[v] in fp64 (gmp_rowdot); out may be a
+    strided column view (e.g. the 4th column of an (n, 4) pack)."""
+    n, d = A.shape
+    if B.shape != A.shape or out.shape[0] != n or B.dtype != A.dtype or out.dtype != A.dtype:
+        raise ValueError("rowdot: A, B (n, d) and out (n,) of one dtype")
+    if A.stride(-1) != 1 or B.stride(-1) != 1:
+        raise ValueError("rowdot: rows must be contiguous")
+    if sub is not None and (sub.dtype != torch.float64 or not sub.is_contiguous()):
+        raise ValueError("rowdot: sub must be a contiguous float64 vector")
+    _lib.check(_lib.load().gmp_rowdot(
+        n, d, _dtype_code(A), A.data_ptr(), _ld(A) if n > 1 else d, B.data_ptr(),
+        _ld(B) if n > 1 else d, sub.data_ptr() if sub is not None else None, out.data_ptr(),
+        int(out.stride(0)), _stream(A.device)), "gmp_rowdot")
+    return out
+
+
 def extrema_backward_binary(g, aux, dZ, phi, role, X, Y, W):
     """Fused max/min backward of a binary message: the gradient of phi's lhs
     (role 0) or rhs (role 1) operand from the winning edges, no (m, d)
