@@ -392,7 +392,15 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
     }
   }
 
-  const int V = pick_v(F, d_out, ops, 2, Z, ldz, ext ? arg : nullptr);
+  int V = pick_v(F, d_out, ops, 2, Z, ldz, ext ? arg : nullptr);
+  // sum / mean into an output whose rows are only 8 B aligned (a column tile
+  // of a row-major Z): keep 16 B gathers, store each 4-vector as two halves
+  int z_split = 0;
+  if (!ext && V < 4 && F == 4 && ldz % 2 == 0 && aligned(Z, 8) &&
+      pick_v(F, d_out, ops, 2, nullptr, 0, nullptr) == 4) {
+    V = 4;
+    z_split = 1;
+  }
   const bool src_full = (ops[0].dev.target == GMP_SRC && !ops[0].dev.bcast) ||
                         (ops[1].present && ops[1].dev.target == GMP_SRC && !ops[1].dev.bcast);
   const int max_tw = 32 * V;
@@ -416,6 +424,7 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
       ncl);
   SpmmArgs a{};
   a.cluster = ncl;
+  a.z_split = z_split;
   a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
   a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_medium;
   a.medium_blocks = medium_blocks; a.blocks_per_tile = bpt_rows;

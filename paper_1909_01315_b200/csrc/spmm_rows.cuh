@@ -101,6 +101,7 @@ struct SpmmArgs {
   const void* attn_pack;  // (n, 4) rows [er, max, inv_sum, w]
   double* attn_t;         // MP_AB: t[u] = sum_{u->v} alpha_e w[v] (nullable)
   int32_t cluster;        // CTAs per heavy row (a thread-block cluster), 1 = one CTA
+  int32_t z_split;        // Z rows only 8 B aligned: store a 4-vector as two 8 B halves
 };
 
 template <typename T>
@@ -729,6 +730,14 @@ __device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_
       double v = acc.acc[k];
       if (a.mean && deg > 0) v = v / (double)deg;  // kernels.py:719-722
       out[k] = (T)v;
+    }
+    if constexpr (V == 4) {
+      if (a.z_split) {  // e.g. a 64-column tile written straight into Z with ld 602
+        const T lo[2] = {out[0], out[1]}, hi[2] = {out[2], out[3]};
+        store_vec<T, 2>(z + col, lo);
+        store_vec<T, 2>(z + col + 2, hi);
+        return;
+      }
     }
     store_vec<T, V>(z + col, out);
   } else {

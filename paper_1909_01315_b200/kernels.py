@@ -425,16 +425,17 @@ def _tiled_applies(phi, rho, X, W, d_out, n, tune):
 
 
 def _gspmm_tiled(g, phi, rho, X, W, Z, d_out):
-    """Aggregation over packed column tiles: gmp_pack_tiles, one gmp_gspmm per
-    256 B tile (each tile's slice of X stays L2-resident while every
-    destination row gathers it; a per-edge scalar is laid out in CSC order
-    once and streamed by every tile), gmp_unpack_tiles into Z."""
+    """Aggregation over packed column tiles: gmp_pack_tiles, then one
+    gmp_gspmm per 256 B tile (each tile's slice of X stays L2-resident while
+    every destination row gathers it; a per-edge scalar is laid out in CSC
+    order once and streamed by every tile) writing its columns of Z in place
+    (16 B vectors stored as two 8 B halves when Z's rows are only 8 B
+    aligned)."""
     lib = _lib.load()
     dev = g.device
     n = g.num_nodes
     F = X.element_size()
     tile = _TILE_BYTES // F
-    vec = 16 // F
     nt = -(-d_out // tile)
     code = _dtype_code(X)
     stream = _stream(dev)
@@ -448,22 +449,17 @@ def _gspmm_tiled(g, phi, rho, X, W, Z, d_out):
         if phi.op == "div":
             err = _err_slot(dev)
     Xp = torch.empty((nt, n, tile), dtype=X.dtype, device=dev)
-    Zp = torch.empty((nt, n, tile), dtype=X.dtype, device=dev)
     _lib.check(lib.gmp_pack_tiles(n, d_out, code, tile, X.data_ptr(), _ld(X), Xp.data_ptr(),
                                   stream), "gmp_pack_tiles")
+    ldz = _ld(Z)
     for t in range(nt):
         w = min(tile, d_out - t * tile)
-        w = -(-w // vec) * vec  # zero-padded columns keep 16 B vectors
         lhs = _lib.GmpOperand(Xp[t].data_ptr(), tile, w, _lib.TARGETS["src"])
-        if rhs is not None:
-            rhs.dim = 1
         _lib.check(lib.gmp_gspmm(ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct),
                                  _lib.OPS[phi.op], _lib.RHOS[rho], code, ctypes.byref(lhs),
-                                 _ptr(rhs), Zp[t].data_ptr(), tile, w, None, None,
+                                 _ptr(rhs), Z.data_ptr() + t * tile * F, ldz, w, None, None,
                                  err.data_ptr() if err is not None else None, None, stream),
                    "gmp_gspmm")
-    _lib.check(lib.gmp_unpack_tiles(n, d_out, code, tile, Zp.data_ptr(), Z.data_ptr(), _ld(Z),
-                                    stream), "gmp_unpack_tiles")
     if err is not None:
         pos = int(err.item())
         if pos != _INT32_MAX:
