@@ -140,6 +140,26 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
               int64_t* arg, int64_t* counts, int32_t* err_pos,
               const gmp_tuning* tuning, void* stream);
 
+/* Staged sum / mean g-SpMM: the rows' edges are split over several
+ * adjacencies (blocks with the same rows - e.g. one per source owner of a
+ * row-partitioned graph, aggregated as each owner's feature shard lands) and
+ * accumulated in one fp64 buffer acc (n_rows, ldacc), rounded once at the
+ * end - the same single rounding as one gmp_gspmm over the union (the
+ * reference accumulates every row in float64, kernels.py:396). Generalises
+ * the reference's node_parallel split of destination ranges
+ * (kernels.py:473-482) to a split of each row's edges.
+ *   GMP_STAGE_FIRST: acc = partial            (Z untouched)
+ *   GMP_STAGE_MID:   acc += partial           (Z untouched)
+ *   GMP_STAGE_LAST:  Z = round(acc + partial) (mean: / deg_full[row])
+ * deg_full (nullable, mean only): the full in-degree of each row over all
+ * stages; NULL = this block's degree. Messages as gmp_gspmm except dot. */
+enum { GMP_STAGE_FIRST = 0, GMP_STAGE_MID = 1, GMP_STAGE_LAST = 3 };
+int gmp_gspmm_staged(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
+                     const gmp_operand* lhs, const gmp_operand* rhs,
+                     double* acc, int64_t ldacc, int mode, const int64_t* deg_full,
+                     void* Z, int64_t ldz, int32_t d_out, int32_t* err_pos,
+                     const gmp_tuning* tuning, void* stream);
+
 /* ---- g-SDDMM ------------------------------------------------------------
  * Replaces kernels.gsddmm (kernels.py:744-836), default strategy
  * edge_parallel over COO (_gsddmm_chunked, kernels.py:732-741):
@@ -201,27 +221,36 @@ int gmp_edge_softmax_uv_stats(const gmp_adj* in_adj, const gmp_sched* sched, int
  * One head of the reference's GAT aggregation (layers.py:110-115: u_add_v ->
  * edge_softmax -> u_mul_e + sum) with the attention weights never stored:
  *   alpha_e = exp((el[src e] + er[dst e]) - max[dst e]) * inv_sum[dst e]
- * pack: (n, 4) rows [er, max, inv_sum, w] (max / inv_sum from
- * gmp_edge_softmax_uv_stats; w is read by the backward only), el: (n) with
- * stride lde.
+ * pack: (n) 32-byte rows, one sector per gathered edge - fp32
+ * [er, max, inv_sum, w_hi, w_lo, 0, 0, 0], fp64 [er, max, inv_sum, w]
+ * (max / inv_sum from gmp_edge_softmax_uv_stats; w = w_hi + w_lo is read by
+ * the backward only, carried to fp64 accuracy), el: (n) with stride lde.
  * backward == 0: adj = in-adjacency, Z[v] = sum_{(u,e)->v} alpha_e X[u]
  * backward == 1: adj = the reverse graph's in-adjacency (= forward CSR),
  *                Z[u] = sum_{(v,e): u->v} alpha_e X[v]  (X = upstream grad rows,
  *                the transposed aggregation of Theorem 1), and, when t_out is
  *                not NULL, t_out[u] = sum_{(v,e): u->v} alpha_e w[v] (fp64) -
  *                the softmax-backward term of d el.
- * X: (n, d) with ldx, Z: (n, d) with ldz. */
+ * X: (n, d) with ldx, Z: (n, d) with ldz. z64 (nullable, (n, d) fp64 with
+ * ldz64): also receives the unrounded fp64 rows of Z, so the backward's row
+ * dots (S_v = dZ[v].Z[v], d el[u] = X[u].dX[u] - t[u]) are formed from the
+ * fp64 aggregate like the reference's float64 composition, not from Z
+ * rounded to fp32 (a cancelling dot would inherit |Z| 2^-24 per term). */
 int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int backward,
                       const void* X, int64_t ldx, int32_t d, const void* el, int64_t lde,
-                      const void* pack, void* Z, int64_t ldz, double* t_out,
-                      const gmp_tuning* tuning, void* stream);
+                      const void* pack, void* Z, int64_t ldz, double* z64, int64_t ldz64,
+                      double* t_out, const gmp_tuning* tuning, void* stream);
 
 /* Node-level epilogue of the fused GAT backward: out[v * out_stride] =
  * sum_c A[v,c] B[v,c] - sub[v] (fp64 accumulation, sub nullable), e.g.
  * S_v = dZ[v].Z[v] straight into the pack's 4th column, and
- * d el[u] = X[u].dX[u] - t[u]. */
-int gmp_rowdot(int64_t n, int32_t d, int dtype, const void* A, int64_t lda, const void* B,
-               int64_t ldb, const double* sub, void* out, int64_t out_stride, void* stream);
+ * d el[u] = X[u].dX[u] - t[u]. A and out have `dtype`; B has b_dtype (dtype,
+ * or GMP_F64 for an fp32 A: the z64 rows of gmp_gat_aggregate). out_pair != 0:
+ * the fp64 result is stored as hi = out[v*out_stride], lo = out[v*out_stride+1]
+ * (the pack's w_hi / w_lo). */
+int gmp_rowdot(int64_t n, int32_t d, int dtype, const void* A, int64_t lda, int b_dtype,
+               const void* B, int64_t ldb, const double* sub, void* out, int64_t out_stride,
+               int out_pair, void* stream);
 
 /* ---- extrema gradient routing ----------------------------------------------
  * Replaces kernels.route_extrema_grad (kernels.py:843-857): dM[arg[v,k], k] =
@@ -230,15 +259,23 @@ int gmp_rowdot(int64_t n, int32_t d, int dtype, const void* A, int64_t lda, cons
 int gmp_route_extrema(int64_t n_rows, int32_t d, int dtype, const int64_t* arg,
                       const void* dZ, int64_t lddz, void* dM, int64_t ldm, void* stream);
 
+/* Workspace bytes of the extrema backward entry points below for n_rows
+ * output rows of cells_per_row cells (d; the operand width for dot). */
+size_t gmp_extrema_bwd_workspace_size(int64_t n_rows, int32_t cells_per_row);
+
 /* Fused max/min backward for copy messages: scatters dZ straight into the
  * gradient of the copied operand without the (m, d) intermediate
  * (autodiff.py:398-412 + _route for copy_lhs/copy_rhs). target_index: for
  * GMP_SRC the COO src array (dX[src[arg]] += dZ), for GMP_EDGE NULL
- * (dW[arg] = dZ). dOut must be zero-filled. Uses atomics for SRC (order of
- * fp additions then varies; tolerance-level parity only). */
+ * (dW[arg] = dZ, one writer per cell). n_target_rows: rows of dOut. dOut
+ * must be zero-filled. Source rows have several writers: their cells are
+ * grouped by a stable radix sort (workspace, gmp_extrema_bwd_workspace_size)
+ * and each (row, column) summed in fp64 in cell order and stored once -
+ * deterministic, no float atomics, one rounding. */
 int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* arg,
                          const void* dZ, int64_t lddz, const int32_t* target_index,
-                         void* dOut, int64_t ldo, void* stream);
+                         int64_t n_target_rows, void* dOut, int64_t ldo, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* Fused max/min backward for binary messages (add / sub / mul / div / dot): the
  * gradient of the lhs (role 0) or rhs (role 1) operand, straight from the
@@ -247,14 +284,18 @@ int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* ar
  * dZ[v,k] * dphi/doperand (fp64, the reference's expression order; 0 where a
  * divisor is 0) to the operand's row src[e] / v / e. own_dim: 1 for a
  * broadcast operand (its cells sum) else d. out (zero-filled by the caller,
- * rows of the operand's target, ldo). Source rows and broadcast operands
- * accumulate with atomics (tolerance-level order); destination and edge
- * rows of full-width operands are written once (bit-exact). dot: d == 1 and
- * own_dim is the operand width (the gradient row is dZ[v] * the other row). */
+ * rows of the operand's target, ldo; n_target_rows of them). Source rows
+ * and broadcast operands have several writers: summed deterministically in
+ * fp64 (sort-grouped as gmp_extrema_bwd_copy; workspace sized by
+ * gmp_extrema_bwd_workspace_size(n_rows, d or own_dim for dot));
+ * destination and edge rows of full-width operands are written once
+ * (bit-exact; workspace may be NULL). dot: d == 1 and own_dim is the operand
+ * width (the gradient row is dZ[v] * the other row). */
 int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dtype,
                            const int64_t* arg, const void* dZ, int64_t lddz, int op, int role,
                            const gmp_operand* lhs, const gmp_operand* rhs, void* out, int64_t ldo,
-                           int32_t own_dim, void* stream);
+                           int32_t own_dim, int64_t n_target_rows, void* workspace,
+                           size_t workspace_bytes, void* stream);
 
 /* ---- row gather ------------------------------------------------------------
  * dst[i, :] = src[idx[i], :] for i < n (dim columns). Used to lay an edge

@@ -18,10 +18,12 @@ OPS = {"copy_lhs": 0, "copy_rhs": 1, "add": 2, "sub": 3, "mul": 4, "div": 5, "do
 TARGETS = {None: -1, "src": 0, "dst": 1, "edge": 2, "edge_pos": 3}
 RHOS = {"sum": 0, "max": 1, "min": 2, "mean": 3}
 GMP_F32, GMP_F64 = 0, 1
+STAGE_FIRST, STAGE_MID, STAGE_LAST = 0, 1, 3
 
-EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "gmp_gsddmm",
+EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "gmp_gspmm_staged",
+            "gmp_gsddmm",
             "gmp_edge_softmax_workspace_size", "gmp_edge_softmax_workspace_size_ex", "gmp_edge_softmax_fwd", "gmp_edge_softmax_uv_fwd", "gmp_edge_softmax_bwd", "gmp_route_extrema",
-            "gmp_extrema_bwd_copy", "gmp_gather_rows", "gmp_neighbor_sample",
+            "gmp_extrema_bwd_workspace_size", "gmp_extrema_bwd_copy", "gmp_gather_rows", "gmp_neighbor_sample",
             "gmp_edge_softmax_uv_stats", "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
             "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
             "gmp_version")
@@ -74,6 +76,9 @@ def _declare(lib):
     lib.gmp_gspmm.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, c_int, c_int,
                               _P(GmpOperand), _P(GmpOperand), vp, i64, i32, vp, vp, vp,
                               _P(GmpTuning), vp]
+    lib.gmp_gspmm_staged.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, c_int, c_int,
+                                     _P(GmpOperand), _P(GmpOperand), vp, i64, c_int, vp, vp, i64,
+                                     i32, vp, _P(GmpTuning), vp]
     lib.gmp_gsddmm.argtypes = [_P(GmpCoo), c_int, c_int, _P(GmpOperand), _P(GmpOperand),
                                vp, i64, i32, vp, vp]
     lib.gmp_edge_softmax_workspace_size.argtypes = [i64, i32]
@@ -87,23 +92,27 @@ def _declare(lib):
     lib.gmp_edge_softmax_bwd.argtypes = [_P(GmpAdj), _P(GmpCoo), _P(GmpSched), c_int, vp, i64, vp,
                                          i64, i32, vp, i64, vp, ctypes.c_size_t, vp]
     lib.gmp_route_extrema.argtypes = [i64, i32, c_int, vp, vp, i64, vp, i64, vp]
-    lib.gmp_extrema_bwd_copy.argtypes = [i64, i32, c_int, vp, vp, i64, vp, vp, i64, vp]
+    lib.gmp_extrema_bwd_workspace_size.argtypes = [i64, i32]
+    lib.gmp_extrema_bwd_workspace_size.restype = ctypes.c_size_t
+    lib.gmp_extrema_bwd_copy.argtypes = [i64, i32, c_int, vp, vp, i64, vp, i64, vp, i64, vp,
+                                         ctypes.c_size_t, vp]
     lib.gmp_gather_rows.argtypes = [i64, i32, c_int, vp, vp, i64, vp, i64, vp]
     lib.gmp_neighbor_sample.argtypes = [vp, i64, vp, i64, vp, ctypes.c_uint64, vp, vp, vp]
     lib.gmp_edge_softmax_uv_stats.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, vp, i64, vp, i64,
                                               i32, vp, ctypes.c_size_t, vp]
     lib.gmp_gat_aggregate.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, c_int, vp, i64, i32, vp,
-                                      i64, vp, vp, i64, vp, _P(GmpTuning), vp]
+                                      i64, vp, vp, i64, vp, i64, vp, _P(GmpTuning), vp]
     lib.gmp_pack_tiles.argtypes = [i64, i32, c_int, i32, vp, i64, vp, vp]
-    lib.gmp_rowdot.argtypes = [i64, i32, c_int, vp, i64, vp, i64, vp, vp, i64, vp]
+    lib.gmp_rowdot.argtypes = [i64, i32, c_int, vp, i64, c_int, vp, i64, vp, vp, i64, c_int, vp]
     lib.gmp_extrema_bwd_binary.argtypes = [_P(GmpCoo), i64, i32, c_int, vp, vp, i64, c_int, c_int,
-                                           _P(GmpOperand), _P(GmpOperand), vp, i64, i32, vp]
+                                           _P(GmpOperand), _P(GmpOperand), vp, i64, i32, i64, vp,
+                                           ctypes.c_size_t, vp]
     lib.gmp_unpack_tiles.argtypes = [i64, i32, c_int, i32, vp, vp, i64, vp]
     lib.gmp_last_error.restype = ctypes.c_char_p
     lib.gmp_strerror.argtypes = [c_int]
     lib.gmp_strerror.restype = ctypes.c_char_p
     lib.gmp_launch_count.restype = ctypes.c_uint64
-    for name in ("gmp_build_schedule", "gmp_gspmm", "gmp_gsddmm", "gmp_edge_softmax_fwd",
+    for name in ("gmp_build_schedule", "gmp_gspmm", "gmp_gspmm_staged", "gmp_gsddmm", "gmp_edge_softmax_fwd",
                  "gmp_edge_softmax_uv_fwd",
                  "gmp_edge_softmax_bwd", "gmp_route_extrema", "gmp_extrema_bwd_copy",
                  "gmp_gather_rows", "gmp_neighbor_sample", "gmp_edge_softmax_uv_stats",

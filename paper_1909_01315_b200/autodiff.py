@@ -325,24 +325,33 @@ class _GATAttention(torch.autograd.Function):
                = X_h[u] . dX_h[u] - sum_{u->v} alpha_e S_v
       d er[v]  = S_v (1 - sum_{e->v} alpha_e) = 0   (softmax is shift-invariant)
     S_v rides in the 4th column of the per-node pack the kernel gathers
-    anyway; the reverse-graph kernel returns t[u] = sum_{u->v} alpha_e S_v."""
+    anyway; the reverse-graph kernel returns t[u] = sum_{u->v} alpha_e S_v.
+    For fp32 features both row dots read the kernels' unrounded fp64 rows
+    (Z64, dX64): S_v and X.dX - t cancel, and a dot of an fp32-rounded row
+    would carry |row| 2^-24 per term into the difference."""
 
     @staticmethod
     def forward(ctx, g, el, er, X, shared):
         H = el.shape[1]
         d = X.shape[1] if shared else X.shape[1] // H
         stat = kernels.edge_softmax_uv_stats(g, el, er)
-        pack = torch.zeros((H, g.num_nodes, 4), dtype=X.dtype, device=X.device)
+        pack = torch.zeros((H, g.num_nodes, kernels.pack_width(X.dtype)), dtype=X.dtype,
+                           device=X.device)
         pack[:, :, 0] = er.t()
         pack[:, :, 1] = stat[:, :H].t()
         pack[:, :, 2] = stat[:, H:].t()
         outs = []
+        z64 = None
+        if X.dtype != torch.float64 and not isinstance(ctx, _NoCtx):
+            z64 = torch.empty((g.num_nodes, H * d), dtype=torch.float64, device=X.device)
         for h in range(H):
             Xh = X if shared else X[:, h * d:(h + 1) * d]
-            outs.append(kernels.gat_aggregate(g, Xh, el[:, h:h + 1], pack[h]))
+            outs.append(kernels.gat_aggregate(
+                g, Xh, el[:, h:h + 1], pack[h],
+                z64=z64[:, h * d:(h + 1) * d] if z64 is not None else None))
         out = outs[0] if H == 1 else torch.cat(outs, dim=1)
         ctx.g, ctx.shared, ctx.d = g, shared, d
-        ctx.save_for_backward(el, er, X, pack, out)
+        ctx.save_for_backward(el, er, X, pack, out if z64 is None else z64)
         return out
 
     @staticmethod
@@ -356,16 +365,19 @@ class _GATAttention(torch.autograd.Function):
             dout = dout.contiguous()
         dX_parts = []
         dEl = torch.empty(el.shape, dtype=X.dtype, device=X.device)
+        dx64 = None
+        if X.dtype != torch.float64:
+            dx64 = torch.empty((g.num_nodes, d), dtype=torch.float64, device=X.device)
         for h in range(H):
             dZh = dout[:, h * d:(h + 1) * d]
-            Zh = out[:, h * d:(h + 1) * d]
+            Zh = out[:, h * d:(h + 1) * d]   # fp64 rows (Z64) for fp32 features
             # S_v = dZ[v].Z[v] (fp64) rides in the pack's 4th column;
             # t[u] = sum_{u->v} alpha_e S_v comes back from the kernel
             pk = pack[h].clone()
-            kernels.rowdot(dZh, Zh, pk[:, 3])
-            dXh, t = kernels.gat_aggregate(g, dZh, el[:, h:h + 1], pk, backward=True)
+            kernels.rowdot(dZh, Zh, pk[:, 3], pair=X.dtype != torch.float64)
+            dXh, t = kernels.gat_aggregate(g, dZh, el[:, h:h + 1], pk, backward=True, z64=dx64)
             Xh = X if shared else X[:, h * d:(h + 1) * d]
-            kernels.rowdot(Xh, dXh, dEl[:, h], sub=t)   # d el = X.dX - t
+            kernels.rowdot(Xh, dXh if dx64 is None else dx64, dEl[:, h], sub=t)  # X.dX - t
             dX_parts.append(dXh)
         if shared:
             dX = dX_parts[0]

@@ -23,7 +23,9 @@ cudaError_t launch_spmm_rows(int, int, int, int, const SpmmArgs&, int64_t, cudaS
 cudaError_t launch_route_extrema(int, int64_t, int32_t, const int64_t*, const void*, int64_t, void*,
                                  int64_t, cudaStream_t);
 cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const void*, int64_t,
-                                    const int32_t*, void*, int64_t, cudaStream_t);
+                                    const int32_t*, int64_t, void*, int64_t, void*, size_t,
+                                    cudaStream_t);
+size_t extrema_workspace_bytes(int64_t cells);
 size_t schedule_workspace_bytes(int64_t n);
 cudaError_t launch_gather_rows(int, int64_t, int32_t, const int32_t*, const void*, int64_t, void*,
                                int64_t, cudaStream_t);
@@ -40,9 +42,9 @@ struct ExtBinArgs {
   int64_t ldo;
   int32_t own_dim;
 };
-cudaError_t launch_extrema_bwd_binary(int, const ExtBinArgs&, cudaStream_t);
-cudaError_t launch_rowdot(int, int64_t, int32_t, const void*, int64_t, const void*, int64_t,
-                          const double*, void*, int64_t, cudaStream_t);
+cudaError_t launch_extrema_bwd_binary(int, const ExtBinArgs&, int64_t, void*, size_t, cudaStream_t);
+cudaError_t launch_rowdot(int, int, int64_t, int32_t, const void*, int64_t, const void*, int64_t,
+                          const double*, void*, int64_t, int, cudaStream_t);
 cudaError_t launch_pack_tiles(int, bool, int64_t, int32_t, int32_t, const void*, int64_t, void*,
                               int64_t, cudaStream_t);
 cudaError_t launch_neighbor_sample(const int64_t*, const int64_t*, int64_t, const int64_t*, uint64_t,
@@ -290,10 +292,17 @@ int gmp_build_schedule(const gmp_adj* adj, int32_t heavy_threshold, int32_t ligh
   return GMP_OK;
 }
 
-int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
-              const gmp_operand* lhs, const gmp_operand* rhs, void* Z, int64_t ldz, int32_t d_out,
-              int64_t* arg, int64_t* counts, int32_t* err_pos, const gmp_tuning* tuning,
-              void* stream) {
+struct Staged {
+  double* acc;
+  int64_t ldacc;
+  int mode;
+  const int64_t* deg_full;
+};
+
+static int gspmm_impl(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
+                      const gmp_operand* lhs, const gmp_operand* rhs, void* Z, int64_t ldz,
+                      int32_t d_out, int64_t* arg, int64_t* counts, int32_t* err_pos,
+                      const gmp_tuning* tuning, void* stream, const Staged* stg) {
   if (!adj) return fail(GMP_EINVAL, "null adjacency");
   if (rho < GMP_SUM || rho > GMP_MEAN) return fail(GMP_EINVAL, "unknown reducer %d", rho);
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
@@ -446,6 +455,9 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
   a.need_eid = ext || (a.lhs.from_eid && a.lhs.mode != M_HOIST) ||
                (ops[1].present && a.rhs.from_eid && a.rhs.mode != M_HOIST);
   a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts; a.err_pos = err_pos;
+  if (stg) {
+    a.acc64 = stg->acc; a.ldacc = stg->ldacc; a.acc_mode = stg->mode; a.deg_full = stg->deg_full;
+  }
   const int64_t grid = bpt_rows * ntiles;
   if (grid >= (1ll << 31)) return fail(GMP_EUNSUPPORTED, "grid too large");
   switch (kop) {
@@ -457,6 +469,33 @@ int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int d
   }
   g_launches++;
   return cuda_status(e, "gmp_gspmm");
+}
+
+int gmp_gspmm(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
+              const gmp_operand* lhs, const gmp_operand* rhs, void* Z, int64_t ldz, int32_t d_out,
+              int64_t* arg, int64_t* counts, int32_t* err_pos, const gmp_tuning* tuning,
+              void* stream) {
+  return gspmm_impl(adj, sched, op, rho, dtype, lhs, rhs, Z, ldz, d_out, arg, counts, err_pos,
+                    tuning, stream, nullptr);
+}
+
+int gmp_gspmm_staged(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
+                     const gmp_operand* lhs, const gmp_operand* rhs, double* acc, int64_t ldacc,
+                     int mode, const int64_t* deg_full, void* Z, int64_t ldz, int32_t d_out,
+                     int32_t* err_pos, const gmp_tuning* tuning, void* stream) {
+  if (rho != GMP_SUM && rho != GMP_MEAN)
+    return fail(GMP_EINVAL, "staged g-SpMM takes sum / mean reducers");
+  if (op == GMP_DOT) return fail(GMP_EUNSUPPORTED, "staged g-SpMM does not take dot messages");
+  if (mode < GMP_STAGE_FIRST || mode > GMP_STAGE_LAST || mode == 2)
+    return fail(GMP_EINVAL, "unknown stage mode %d", mode);
+  if (!adj) return fail(GMP_EINVAL, "null adjacency");
+  if (adj->n_rows > 0 && d_out > 0 && (!acc || ldacc < d_out))
+    return fail(GMP_EINVAL, "bad fp64 accumulator / ldacc");
+  const int flags = mode == GMP_STAGE_FIRST ? kAccStore
+                  : mode == GMP_STAGE_MID ? (kAccRead | kAccStore) : (kAccRead | kAccZ);
+  Staged st{acc, ldacc, flags, deg_full};
+  return gspmm_impl(adj, sched, op, rho, dtype, lhs, rhs, Z, ldz, d_out, nullptr, nullptr,
+                    err_pos, tuning, stream, &st);
 }
 
 int gmp_gsddmm(const gmp_coo* coo, int op, int dtype, const gmp_operand* lhs, const gmp_operand* rhs,
@@ -680,16 +719,27 @@ int gmp_route_extrema(int64_t n_rows, int32_t d, int dtype, const int64_t* arg, 
   return cuda_status(e, "gmp_route_extrema");
 }
 
+size_t gmp_extrema_bwd_workspace_size(int64_t n_rows, int32_t cells_per_row) {
+  if (n_rows <= 0 || cells_per_row <= 0) return 0;
+  return extrema_workspace_bytes(n_rows * (int64_t)cells_per_row);
+}
+
 int gmp_extrema_bwd_copy(int64_t n_rows, int32_t d, int dtype, const int64_t* arg, const void* dZ,
-                         int64_t lddz, const int32_t* target_index, void* dOut, int64_t ldo,
+                         int64_t lddz, const int32_t* target_index, int64_t n_target_rows,
+                         void* dOut, int64_t ldo, void* workspace, size_t workspace_bytes,
                          void* stream) {
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
-  if (n_rows < 0 || d < 0 || lddz < d || ldo < d) return fail(GMP_EINVAL, "bad sizes");
+  if (n_rows < 0 || d < 0 || lddz < d || ldo < d || n_target_rows < 0)
+    return fail(GMP_EINVAL, "bad sizes");
   if (n_rows == 0 || d == 0) return GMP_OK;
   if (!arg || !dZ || !dOut) return fail(GMP_EINVAL, "null arrays");
+  if (target_index && (!workspace || workspace_bytes < gmp_extrema_bwd_workspace_size(n_rows, d)))
+    return fail(GMP_EINVAL, "workspace too small: %zu < %zu", workspace_bytes,
+                gmp_extrema_bwd_workspace_size(n_rows, d));
   cudaError_t e = launch_extrema_bwd_copy(dtype == GMP_F64, n_rows, d, arg, dZ, lddz, target_index,
-                                          dOut, ldo, (cudaStream_t)stream);
-  g_launches++;
+                                          n_target_rows, dOut, ldo, workspace, workspace_bytes,
+                                          (cudaStream_t)stream);
+  g_launches += target_index ? 3 : 1;
   return cuda_status(e, "gmp_extrema_bwd_copy");
 }
 
@@ -703,19 +753,20 @@ int gmp_edge_softmax_uv_stats(const gmp_adj* in_adj, const gmp_sched* sched, int
 
 int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int backward,
                       const void* X, int64_t ldx, int32_t d, const void* el, int64_t lde,
-                      const void* pack, void* Z, int64_t ldz, double* t_out,
-                      const gmp_tuning* tuning, void* stream) {
+                      const void* pack, void* Z, int64_t ldz, double* z64, int64_t ldz64,
+                      double* t_out, const gmp_tuning* tuning, void* stream) {
   if (!adj) return fail(GMP_EINVAL, "null adjacency");
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
   if (adj->m < 0 || adj->m >= (1ll << 31)) return fail(GMP_EINVAL, "edge count out of int32 range");
   if (adj->n_rows < 0 || adj->n_rows >= (1ll << 31)) return fail(GMP_EINVAL, "row count out of range");
-  if (d < 0 || ldx < d || ldz < d || lde < 1 || ldx >= (1ll << 32) || lde >= (1ll << 32))
+  if (d < 0 || ldx < d || ldz < d || lde < 1 || ldx >= (1ll << 32) || lde >= (1ll << 32) ||
+      (z64 && ldz64 < d))
     return fail(GMP_EINVAL, "bad sizes / leading dimensions");
   if (adj->n_rows == 0 || d == 0) return GMP_OK;
   if (!X || !el || !pack || !Z || !adj->indptr || (adj->m > 0 && !adj->indices))
     return fail(GMP_EINVAL, "null arrays");
   const size_t F = dtype == GMP_F64 ? 8 : 4;
-  if (!aligned(pack, 4 * F)) return fail(GMP_EINVAL, "pack must be aligned to a 4-element row");
+  if (!aligned(pack, 32)) return fail(GMP_EINVAL, "pack must be aligned to its 32-byte rows");
   if (sched && sched->order == nullptr && sched->n_heavy > 0)
     return fail(GMP_EINVAL, "schedule has heavy rows but no order");
   Opnd ops[2] = {};
@@ -749,6 +800,9 @@ int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int
   a.Z = Z; a.ldz = ldz;
   a.attn_el = el; a.attn_lde = (uint32_t)lde; a.attn_pack = pack;
   a.attn_t = backward ? t_out : nullptr;
+  if (z64) {  // the unrounded fp64 rows too (exact operand of the backward's row dots)
+    a.acc64 = z64; a.ldacc = ldz64; a.acc_mode = kAccZ | kAccStore;
+  }
   const int64_t grid = bpt_rows * ntiles;
   if (grid >= (1ll << 31)) return fail(GMP_EUNSUPPORTED, "grid too large");
   cudaError_t e = launch_spmm_rows_attn(F == 8, V, backward != 0, a, grid, (cudaStream_t)stream);
@@ -783,7 +837,8 @@ int gmp_unpack_tiles(int64_t n, int32_t d, int dtype, int32_t tile, const void* 
 int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dtype,
                            const int64_t* arg, const void* dZ, int64_t lddz, int op, int role,
                            const gmp_operand* lhs, const gmp_operand* rhs, void* out, int64_t ldo,
-                           int32_t own_dim, void* stream) {
+                           int32_t own_dim, int64_t n_target_rows, void* workspace,
+                           size_t workspace_bytes, void* stream) {
   if (!coo || !lhs || !rhs) return fail(GMP_EINVAL, "null coo / operand");
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
   if (op != GMP_ADD && op != GMP_SUB && op != GMP_MUL && op != GMP_DIV && op != GMP_DOT)
@@ -808,19 +863,28 @@ int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dt
   a.lhs = to_dev(lhs, op == GMP_DOT ? lhs->dim : d).dev;
   a.rhs = to_dev(rhs, op == GMP_DOT ? rhs->dim : d).dev;
   a.out = out; a.ldo = ldo; a.own_dim = own_dim;
-  cudaError_t e = launch_extrema_bwd_binary(dtype == GMP_F64, a, (cudaStream_t)stream);
-  g_launches++;
+  const bool many = own->target == GMP_SRC || (op != GMP_DOT && own_dim == 1);
+  const int32_t cells = op == GMP_DOT ? own_dim : d;
+  if (n_target_rows < 0) return fail(GMP_EINVAL, "bad sizes");
+  if (many && (!workspace || workspace_bytes < gmp_extrema_bwd_workspace_size(n_rows, cells)))
+    return fail(GMP_EINVAL, "workspace too small: %zu < %zu", workspace_bytes,
+                gmp_extrema_bwd_workspace_size(n_rows, cells));
+  cudaError_t e = launch_extrema_bwd_binary(dtype == GMP_F64, a, n_target_rows, workspace,
+                                            workspace_bytes, (cudaStream_t)stream);
+  g_launches += many ? 3 : 1;
   return cuda_status(e, "gmp_extrema_bwd_binary");
 }
 
-int gmp_rowdot(int64_t n, int32_t d, int dtype, const void* A, int64_t lda, const void* B,
-               int64_t ldb, const double* sub, void* out, int64_t out_stride, void* stream) {
+int gmp_rowdot(int64_t n, int32_t d, int dtype, const void* A, int64_t lda, int b_dtype,
+               const void* B, int64_t ldb, const double* sub, void* out, int64_t out_stride,
+               int out_pair, void* stream) {
   if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (b_dtype != dtype && b_dtype != GMP_F64) return fail(GMP_EINVAL, "B must be dtype or f64");
   if (n < 0 || d < 0 || lda < d || ldb < d || out_stride < 1) return fail(GMP_EINVAL, "bad sizes");
   if (n == 0) return GMP_OK;
   if ((d > 0 && (!A || !B)) || !out) return fail(GMP_EINVAL, "null arrays");
-  cudaError_t e = launch_rowdot(dtype == GMP_F64, n, d, A, lda, B, ldb, sub, out, out_stride,
-                                (cudaStream_t)stream);
+  cudaError_t e = launch_rowdot(dtype == GMP_F64, b_dtype == GMP_F64, n, d, A, lda, B, ldb, sub,
+                                out, out_stride, out_pair ? 1 : 0, (cudaStream_t)stream);
   g_launches++;
   return cuda_status(e, "gmp_rowdot");
 }

@@ -223,20 +223,94 @@ __global__ void route_extrema_kernel(int64_t n, int32_t d, const int64_t* __rest
   }
 }
 
+// ---- deterministic many-writer accumulation ----------------------------------
+// Cells whose gradient row has several writers (a source row that wins
+// several (row, column) cells, a broadcast operand) emit (key = out row *
+// cols + out column, fp64 value) pairs; a stable radix sort groups them by
+// key in cell order and one thread per key sums its run in fp64 and stores
+// the rounded result once. Same terms, same order every run - no float
+// atomics, one rounding (the reference routes then reduces in float64,
+// kernels.py:843-857 + autodiff.py:398-412).
+struct CellSink {
+  uint64_t* keys;  // null: single-writer targets store directly
+  double* vals;
+};
+
+int key_bits(uint64_t max_key) {
+  int b = 1;
+  while (b < 64 && (max_key >> b)) ++b;
+  return b;
+}
+
+template <typename T>
+__global__ void segment_sum_kernel(int64_t total, const uint64_t* __restrict__ ks,
+                                   const double* __restrict__ vs, uint64_t inv, int64_t cols,
+                                   T* out, int64_t ldo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = ks[i];
+    if (key == inv || (i > 0 && ks[i - 1] == key)) continue;  // invalid, or not a run head
+    double acc = 0.0;
+    for (int64_t j = i; j < total && ks[j] == key; ++j) acc += vs[j];
+    const int64_t row = (int64_t)(key / (uint64_t)cols), col = (int64_t)(key % (uint64_t)cols);
+    out[row * ldo + col] = (T)acc;
+  }
+}
+
+size_t extrema_cub_bytes(int64_t cells) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs((void*)nullptr, bytes, (const uint64_t*)nullptr,
+                                  (uint64_t*)nullptr, (const double*)nullptr, (double*)nullptr,
+                                  (int)std::max<int64_t>(cells, 1));
+  return bytes;
+}
+
+static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t extrema_workspace_bytes(int64_t cells) {
+  if (cells <= 0) return 0;
+  return 4 * al256((size_t)cells * 8) + al256(extrema_cub_bytes(cells));
+}
+
+// sort the emitted pairs and store one fp64 sum per key
+template <typename T>
+cudaError_t sort_and_sum(int64_t cells, void* ws, size_t ws_bytes, uint64_t inv, int64_t cols,
+                         T* out, int64_t ldo, cudaStream_t s) {
+  char* p = static_cast<char*>(ws);
+  uint64_t* k0 = reinterpret_cast<uint64_t*>(p);
+  double* v0 = reinterpret_cast<double*>(p + al256((size_t)cells * 8));
+  uint64_t* k1 = reinterpret_cast<uint64_t*>(p + 2 * al256((size_t)cells * 8));
+  double* v1 = reinterpret_cast<double*>(p + 3 * al256((size_t)cells * 8));
+  char* tmp = p + 4 * al256((size_t)cells * 8);
+  size_t tmp_bytes = ws_bytes - 4 * al256((size_t)cells * 8);
+  // invalid cells carry inv (all ones over the sorted bits): they land last
+  const int bits = key_bits(inv);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, (int)cells, 0,
+                                                  bits, s);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)std::min<int64_t>((cells + 255) / 256, 148 * 32);
+  segment_sum_kernel<T><<<grid, 256, 0, s>>>(cells, k1, v1, inv, cols, out, ldo);
+  return cudaGetLastError();
+}
+
 template <typename T>
 __global__ void extrema_bwd_copy_kernel(int64_t n, int32_t d, const int64_t* __restrict__ arg,
                                         const T* __restrict__ dZ, int64_t lddz,
-                                        const int32_t* __restrict__ tindex, T* dOut, int64_t ldo) {
+                                        const int32_t* __restrict__ tindex, T* dOut, int64_t ldo,
+                                        CellSink sink, uint64_t max_key) {
   const int64_t total = n * (int64_t)d;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = i / d;
     const int k = (int)(i - v * d);
     const int64_t e = arg[i];
-    if (e < 0) continue;
-    const T g = dZ[v * lddz + k];
-    if (tindex) atomicAdd(dOut + (int64_t)tindex[e] * ldo + k, g);
-    else dOut[e * ldo + k] = g;  // one winner per (edge, column)
+    if (tindex) {  // dX[src[e]]: many writers
+      // keys of invalid cells: all ones in the sorted bit range (> every real key)
+      sink.keys[i] = e < 0 ? max_key : (uint64_t)tindex[e] * (uint64_t)d + (uint64_t)k;
+      sink.vals[i] = e < 0 ? 0.0 : (double)dZ[v * lddz + k];
+      continue;
+    }
+    if (e >= 0) dOut[e * ldo + k] = dZ[v * lddz + k];  // one winner per (edge, column)
   }
 }
 
@@ -250,15 +324,33 @@ cudaError_t launch_route_extrema(int f64, int64_t n, int32_t d, const int64_t* a
   return cudaGetLastError();
 }
 
+// max_key: an upper bound on real keys (target rows * d); invalid cells get
+// the all-ones pattern of the sorted bit range so they sort last
+static uint64_t invalid_key(uint64_t max_key) {
+  const int bits = key_bits(max_key + 1);
+  return bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+}
+
 cudaError_t launch_extrema_bwd_copy(int f64, int64_t n, int32_t d, const int64_t* arg,
                                     const void* dZ, int64_t lddz, const int32_t* tindex,
-                                    void* dOut, int64_t ldo, cudaStream_t s) {
+                                    int64_t n_target_rows, void* dOut, int64_t ldo, void* ws,
+                                    size_t ws_bytes, cudaStream_t s) {
   const int64_t total = n * (int64_t)d;
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
   if (total == 0) return cudaSuccess;
-  if (f64) extrema_bwd_copy_kernel<double><<<grid, 256, 0, s>>>(n, d, arg, (const double*)dZ, lddz, tindex, (double*)dOut, ldo);
-  else extrema_bwd_copy_kernel<float><<<grid, 256, 0, s>>>(n, d, arg, (const float*)dZ, lddz, tindex, (float*)dOut, ldo);
-  return cudaGetLastError();
+  CellSink sink{nullptr, nullptr};
+  const uint64_t max_key = (uint64_t)n_target_rows * (uint64_t)d;
+  const uint64_t inv = invalid_key(max_key);
+  if (tindex) {
+    sink.keys = static_cast<uint64_t*>(ws);
+    sink.vals = reinterpret_cast<double*>(static_cast<char*>(ws) + al256((size_t)total * 8));
+  }
+  if (f64) extrema_bwd_copy_kernel<double><<<grid, 256, 0, s>>>(n, d, arg, (const double*)dZ, lddz, tindex, (double*)dOut, ldo, sink, inv);
+  else extrema_bwd_copy_kernel<float><<<grid, 256, 0, s>>>(n, d, arg, (const float*)dZ, lddz, tindex, (float*)dOut, ldo, sink, inv);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !tindex) return e;
+  return f64 ? sort_and_sum<double>(total, ws, ws_bytes, inv, d, (double*)dOut, ldo, s)
+             : sort_and_sum<float>(total, ws, ws_bytes, inv, d, (float*)dOut, ldo, s);
 }
 
 // Fused max/min backward of a binary message (add / sub / mul / div of two
@@ -291,7 +383,7 @@ __device__ __forceinline__ int64_t ext_row(int32_t t, int64_t u, int64_t v, int6
 // dot messages (d_out == 1): cell (v, c) for every operand column c adds
 // dZ[v] * other[c] to the operand's row (d(a.b)/da = b)
 template <typename T>
-__global__ void extrema_bwd_dot_kernel(const ExtBinArgs a) {
+__global__ void extrema_bwd_dot_kernel(const ExtBinArgs a, CellSink sink, uint64_t inv) {
   const int64_t total = a.n * (int64_t)a.own_dim;
   T* out = static_cast<T*>(a.out);
   const OperandDev& other = a.role == 0 ? a.rhs : a.lhs;
@@ -300,19 +392,25 @@ __global__ void extrema_bwd_dot_kernel(const ExtBinArgs a) {
     const int64_t v = i / a.own_dim;
     const int c = (int)(i - v * a.own_dim);
     const int64_t e = a.arg[v];
-    if (e < 0) continue;
+    if (e < 0) {
+      if (sink.keys) { sink.keys[i] = inv; sink.vals[i] = 0.0; }
+      continue;
+    }
     const int64_t u = __ldg(a.src + e);
     const double dz = (double)static_cast<const T*>(a.dZ)[v * a.lddz];
     const double ov = (double)static_cast<const T*>(other.data)[
         ext_row(other.target, u, v, e) * other.ld + c];
-    T* dst = out + ext_row(a.target, u, v, e) * a.ldo + c;
-    if (a.target == T_SRC) atomicAdd(dst, (T)(dz * ov));
-    else *dst = (T)(dz * ov);
+    if (sink.keys) {  // source rows: many writers
+      sink.keys[i] = (uint64_t)u * (uint64_t)a.own_dim + (uint64_t)c;
+      sink.vals[i] = dz * ov;
+    } else {
+      out[ext_row(a.target, u, v, e) * a.ldo + c] = (T)(dz * ov);
+    }
   }
 }
 
 template <typename T>
-__global__ void extrema_bwd_binary_kernel(const ExtBinArgs a) {
+__global__ void extrema_bwd_binary_kernel(const ExtBinArgs a, CellSink sink, uint64_t inv) {
   const int64_t total = a.n * (int64_t)a.d;
   T* out = static_cast<T*>(a.out);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -320,7 +418,10 @@ __global__ void extrema_bwd_binary_kernel(const ExtBinArgs a) {
     const int64_t v = i / a.d;
     const int k = (int)(i - v * a.d);
     const int64_t e = a.arg[i];
-    if (e < 0) continue;
+    if (e < 0) {
+      if (sink.keys) { sink.keys[i] = inv; sink.vals[i] = 0.0; }
+      continue;
+    }
     const int64_t u = __ldg(a.src + e);
     const double dz = (double)static_cast<const T*>(a.dZ)[v * a.lddz + k];
     const double av = (double)static_cast<const T*>(a.lhs.data)[
@@ -338,54 +439,74 @@ __global__ void extrema_bwd_binary_kernel(const ExtBinArgs a) {
         break;
     }
     const int64_t row = ext_row(a.target, u, v, e);
-    T* dst = out + row * a.ldo + (a.own_dim == 1 ? 0 : k);
-    if (a.target == T_SRC || a.own_dim == 1) atomicAdd(dst, (T)g);
-    else *dst = (T)g;
+    const int col = a.own_dim == 1 ? 0 : k;
+    if (sink.keys) {  // source rows / broadcast operands: many writers
+      sink.keys[i] = (uint64_t)row * (uint64_t)a.own_dim + (uint64_t)col;
+      sink.vals[i] = g;
+    } else {
+      out[row * a.ldo + col] = (T)g;  // one cell per (row, column)
+    }
   }
 }
 
-cudaError_t launch_extrema_bwd_binary(int f64, const ExtBinArgs& a, cudaStream_t s) {
-  if (a.op == OP_DOT) {
-    const int64_t total = a.n * (int64_t)a.own_dim;
-    if (total == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
-    if (f64) extrema_bwd_dot_kernel<double><<<grid, 256, 0, s>>>(a);
-    else extrema_bwd_dot_kernel<float><<<grid, 256, 0, s>>>(a);
-    return cudaGetLastError();
-  }
-  const int64_t total = a.n * (int64_t)a.d;
+cudaError_t launch_extrema_bwd_binary(int f64, const ExtBinArgs& a, int64_t n_target_rows,
+                                      void* ws, size_t ws_bytes, cudaStream_t s) {
+  const bool dot = a.op == OP_DOT;
+  const int64_t total = a.n * (int64_t)(dot ? a.own_dim : a.d);
   if (total == 0) return cudaSuccess;
+  const bool many = a.target == T_SRC || (!dot && a.own_dim == 1);
+  CellSink sink{nullptr, nullptr};
+  const uint64_t inv = invalid_key((uint64_t)n_target_rows * (uint64_t)a.own_dim);
+  if (many) {
+    sink.keys = static_cast<uint64_t*>(ws);
+    sink.vals = reinterpret_cast<double*>(static_cast<char*>(ws) + al256((size_t)total * 8));
+  }
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
-  if (f64) extrema_bwd_binary_kernel<double><<<grid, 256, 0, s>>>(a);
-  else extrema_bwd_binary_kernel<float><<<grid, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  if (dot) {
+    if (f64) extrema_bwd_dot_kernel<double><<<grid, 256, 0, s>>>(a, sink, inv);
+    else extrema_bwd_dot_kernel<float><<<grid, 256, 0, s>>>(a, sink, inv);
+  } else {
+    if (f64) extrema_bwd_binary_kernel<double><<<grid, 256, 0, s>>>(a, sink, inv);
+    else extrema_bwd_binary_kernel<float><<<grid, 256, 0, s>>>(a, sink, inv);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !many) return e;
+  return f64 ? sort_and_sum<double>(total, ws, ws_bytes, inv, a.own_dim, (double*)a.out, a.ldo, s)
+             : sort_and_sum<float>(total, ws, ws_bytes, inv, a.own_dim, (float*)a.out, a.ldo, s);
 }
 
 // ---- row dot products: out[v * os] = sum_c A[v,c] B[v,c] - sub[v] (fp64) ---------
 // The fused GAT backward's node-level epilogue (S_v = dZ[v].Z[v] into the
 // pack; d el[u] = X[u].dX[u] - t[u]) in one pass each instead of a chain of
 // elementwise / reduction launches.
-template <typename T>
+template <typename T, typename TB>
 __global__ void rowdot_kernel(int64_t n, int32_t d, const T* __restrict__ A, int64_t lda,
-                              const T* __restrict__ B, int64_t ldb,
-                              const double* __restrict__ sub, T* out, int64_t os) {
+                              const TB* __restrict__ B, int64_t ldb,
+                              const double* __restrict__ sub, T* out, int64_t os, int pair) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     double acc = 0.0;
     const T* a = A + v * lda;
-    const T* b = B + v * ldb;
+    const TB* b = B + v * ldb;
     for (int c = 0; c < d; ++c) acc += (double)__ldg(a + c) * (double)__ldg(b + c);
     if (sub) acc -= sub[v];
-    out[v * os] = (T)acc;
+    const T hi = (T)acc;
+    out[v * os] = hi;
+    if (pair) out[v * os + 1] = (T)(acc - (double)hi);  // fp64 value as hi + lo
   }
 }
 
-cudaError_t launch_rowdot(int f64, int64_t n, int32_t d, const void* A, int64_t lda, const void* B,
-                          int64_t ldb, const double* sub, void* out, int64_t os, cudaStream_t s) {
+// B may be fp64 for an fp32 A: the unrounded fp64 rows of an aggregation
+// (gmp_gat_aggregate's z64), so a dot that cancels is not limited by the
+// fp32 rounding of B
+cudaError_t launch_rowdot(int f64, int b_f64, int64_t n, int32_t d, const void* A, int64_t lda,
+                          const void* B, int64_t ldb, const double* sub, void* out, int64_t os,
+                          int pair, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
-  if (f64) rowdot_kernel<double><<<grid, 256, 0, s>>>(n, d, (const double*)A, lda, (const double*)B, ldb, sub, (double*)out, os);
-  else rowdot_kernel<float><<<grid, 256, 0, s>>>(n, d, (const float*)A, lda, (const float*)B, ldb, sub, (float*)out, os);
+  if (f64) rowdot_kernel<double, double><<<grid, 256, 0, s>>>(n, d, (const double*)A, lda, (const double*)B, ldb, sub, (double*)out, os, pair);
+  else if (b_f64) rowdot_kernel<float, double><<<grid, 256, 0, s>>>(n, d, (const float*)A, lda, (const double*)B, ldb, sub, (float*)out, os, pair);
+  else rowdot_kernel<float, float><<<grid, 256, 0, s>>>(n, d, (const float*)A, lda, (const float*)B, ldb, sub, (float*)out, os, pair);
   return cudaGetLastError();
 }
 

@@ -59,19 +59,8 @@ struct SoftmaxArgs {
 };
 
 
-// exp(x - m) of a softmax term. fp32: 2^((x - m) log2 e) on the SFU
-// (ex2.approx.ftz, max rel. error 2^-22; the FFMA-formed argument adds
-// |x - m| * 2^-24 relative - below 1e-6 for any term >= 1e-6 of its row's
-// max, results below 2^-126 flush to zero). Every fp32 softmax term in the
-// library (statistics, normalisation, fused GAT weights) uses this one
-// formula, so a row's weights sum to 1 up to the rounding of the terms.
-constexpr float kLog2e = 1.4426950408889634f;
-__device__ __forceinline__ float softmax_exp(float x, float m) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmaf_rn(x, kLog2e, -m * kLog2e)));
-  return y;
-}
-__device__ __forceinline__ double softmax_exp(double x, double m) { return exp(x - m); }
+// exp(x - m) of a softmax term: sm_exp / uv_score in spmm_rows.cuh (error
+// relative to |x - m|, one formula for every fp32 softmax term).
 
 // (m, l) online-softmax merge in fp64 for l; empty partials carry m = -inf.
 template <typename T>
@@ -80,8 +69,8 @@ __device__ __forceinline__ void sm_merge(T& m, double& l, T om, double ol) {
   if (m == -INFINITY) { m = om; l = ol; return; }
   // the rescale factor in the element precision: its error (~1 ulp of the
   // fp32 exponent difference) is weighted by the factor itself, < 3e-8 of l
-  if (om > m) { l = l * (double)softmax_exp(m, om) + ol; m = om; }
-  else        { l += ol * (double)softmax_exp(om, m); }
+  if (om > m) { l = l * (double)sm_exp(m, om) + ol; m = om; }
+  else        { l += ol * (double)sm_exp(om, m); }
 }
 
 // per-column running sum: compensated fp32 pair for float, plain fp64 for double
@@ -151,6 +140,7 @@ __device__ __forceinline__ void stats_pass1(const SoftmaxArgs& a, const int32_t*
     fetch(cb + stride);
     for (int t = 0; t < cnt; t += E * U) {
       T x[U][V], gg[U][V];
+      T xl[UV ? U : 1][V];  // UV: low part of the exact score el + er
       bool ok[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -159,10 +149,16 @@ __device__ __forceinline__ void stats_pass1(const SoftmaxArgs& a, const int32_t*
         const int64_t e = buf[j & (kChunk - 1)];
 #pragma unroll
         for (int k = 0; k < V; ++k) x[u][k] = gg[u][k] = T(0);
+        if constexpr (UV) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) xl[u][k] = T(0);
+        }
         if (UV && ok[u]) {  // e is the source node: score = el[u] + er[row]
           load_vec<T, V>(EL + e * a.lde, x[u]);
 #pragma unroll
-          for (int k = 0; k < V; ++k) x[u][k] = x[u][k] + er_row[k];
+          for (int k = 0; k < V; ++k) {
+            if constexpr (UV) uv_score(x[u][k], er_row[k], x[u][k], xl[u][k]);
+          }
         } else if (ok[u]) {
           load_vec<T, V>(S + e * a.lds, x[u]);
           if constexpr (BWD) load_vec<T, V>(Gd + e * a.ldg, gg[u]);
@@ -185,12 +181,15 @@ __device__ __forceinline__ void stats_pass1(const SoftmaxArgs& a, const int32_t*
           for (int u = 0; u < U; ++u)
             if (ok[u] && x[u][k] > mx) mx = x[u][k];
           if (mx > m[k]) {
-            if (m[k] != T(-INFINITY)) acc[k].scale(softmax_exp(m[k], mx));
+            if (m[k] != T(-INFINITY)) acc[k].scale(sm_exp(m[k], mx));
             m[k] = mx;
           }
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (ok[u]) acc[k].add(softmax_exp(x[u][k], m[k]));
+          for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            if constexpr (UV) acc[k].add(sm_exp(x[u][k], xl[u][k], m[k]));
+            else acc[k].add(sm_exp(x[u][k], m[k]));
+          }
         }
       }
     }
@@ -466,7 +465,7 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
 #pragma unroll
     for (int u = 0; u < kApplyU; ++u) { vc[u] = vn[u]; uc[u] = UV ? un[u] : 0; }
     fetch_ids(i0 + step);
-    T x[kApplyU][V], gg[kApplyU][V], p0[kApplyU][V], p1[kApplyU][V];
+    T x[kApplyU][V], xl[kApplyU][V], gg[kApplyU][V], p0[kApplyU][V], p1[kApplyU][V];
     int64_t ev[kApplyU];
     int cv[kApplyU];
     bool ok[kApplyU];
@@ -484,7 +483,7 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
         load_vec<T, V>(static_cast<const T*>(a.el) + (int64_t)uc[u] * a.lde + c, x[u]);
         load_vec<T, V>(static_cast<const T*>(a.er) + v * a.ldr + c, xr);
 #pragma unroll
-        for (int k = 0; k < V; ++k) x[u][k] = x[u][k] + xr[k];
+        for (int k = 0; k < V; ++k) uv_score(x[u][k], xr[k], x[u][k], xl[u][k]);
       } else {
         load_vec<T, V>(static_cast<const T*>(a.s) + e * a.lds + c, x[u]);
       }
@@ -511,7 +510,8 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
             r[k] = (T)__fmaf_rn((float)x[u][k], dh, __fmul_rn((float)x[u][k], dc));
           }
         } else {
-          r[k] = softmax_exp(x[u][k], p0[u][k]) * p1[u][k];
+          if constexpr (UV) r[k] = sm_exp(x[u][k], xl[u][k], p0[u][k]) * p1[u][k];
+          else r[k] = sm_exp(x[u][k], p0[u][k]) * p1[u][k];
         }
       }
       store_vec<T, V>(static_cast<T*>(a.out) + ev[u] * a.ldo + cv[u], r);

@@ -74,6 +74,8 @@ struct RowOperand {
   int32_t from_pos;  // edge operand already permuted to adjacency order: row = position
 };
 
+enum { kAccRead = 1, kAccZ = 2, kAccStore = 4 };
+
 struct SpmmArgs {
   const int64_t* indptr;
   const int32_t* indices;
@@ -98,10 +100,29 @@ struct SpmmArgs {
   // fused attention (MP_AF / MP_AB only)
   const void* attn_el;    // (n) el column, stride attn_lde
   uint32_t attn_lde;
-  const void* attn_pack;  // (n, 4) rows [er, max, inv_sum, w]
+  const void* attn_pack;  // (n, PackW<T>) 32 B rows [er, max, inv_sum, w (, w_lo)]
   double* attn_t;         // MP_AB: t[u] = sum_{u->v} alpha_e w[v] (nullable)
   int32_t cluster;        // CTAs per heavy row (a thread-block cluster), 1 = one CTA
   int32_t z_split;        // Z rows only 8 B aligned: store a 4-vector as two 8 B halves
+  // fp64 row sums (sum / mean only; null acc64: plain store of Z). acc_mode
+  // bits: kAccRead - add acc64[row] first (staged sums over several edge
+  // blocks of the same rows, gmp_gspmm_staged); kAccZ - round once into Z
+  // (mean divides by deg_full[row] when given); kAccStore - store the fp64
+  // sum into acc64 (a later stage, or an exact copy of Z for the fused GAT
+  // backward's row dots).
+  double* acc64;
+  int64_t ldacc;
+  int32_t acc_mode;
+  const int64_t* deg_full;
+};
+
+// per-node pack of the fused attention: one 32 B row (a single sector per
+// gathered edge): fp32 [er, max, inv_sum, w_hi, w_lo, -, -, -], fp64
+// [er, max, inv_sum, w]. w = S_v (backward only) is carried to fp64
+// accuracy: t[u] = sum alpha_e S_v feeds d el = X.dX - t, which cancels.
+template <typename T>
+struct PackW {
+  static constexpr int value = sizeof(T) == 4 ? 8 : 4;
 };
 
 template <typename T>
@@ -124,38 +145,73 @@ __device__ __forceinline__ void attn_row_consts(const SpmmArgs& a, int64_t row, 
   if (row < 0) return;
   if constexpr (MP == MP_AF) {
     T w;
-    load_pack4<T>(static_cast<const T*>(a.attn_pack) + row * 4, rc[0], rc[1], rc[2], w);
+    load_pack4<T>(static_cast<const T*>(a.attn_pack) + row * PackW<T>::value, rc[0], rc[1], rc[2],
+                  w);
   } else if constexpr (MP == MP_AB) {
     rc[0] = __ldg(static_cast<const T*>(a.attn_el) + (uint64_t)row * a.attn_lde);
   }
 }
 
-// exp(x - m) of an attention weight: the same formula as softmax.cuh's
-// softmax_exp (2^((x - m) log2 e) on the SFU for fp32), so a recomputed
-// weight equals the one the normalisation kernel would store, bit for bit
-constexpr float kAttnLog2e = 1.4426950408889634f;
-__device__ __forceinline__ float attn_exp(float x, float m) {
+// exp(x - m) of a softmax term / attention weight. fp32: 2^((x - m) log2 e)
+// on the SFU (ex2.approx.ftz, max rel. error 2^-22). The argument is formed
+// as (x - m) first and then scaled, so its rounding error is relative to
+// |x - m| (x - m is exact by Sterbenz whenever x and m are within a factor 2
+// of each other, i.e. for every term that is not negligible), never to |m|:
+// rounding -m*log2e first would put an absolute exponent error of
+// ulp(m log2e)/2 on every term, 2.4e-5 relative at |m| ~ 1000, which does not
+// cancel once partials with different maxima are merged. u_add_v scores
+// (GAT) are carried as the exact TwoSum pair hi + lo of el + er and enter as
+// ((hi - m) + lo), so the fp32 rounding of the score itself (|s| 2^-24) does
+// not leak into the exponent either. Every fp32 softmax term in the library
+// (statistics, rescale, merges, normalisation, fused GAT weights) uses these
+// formulas, so a recomputed weight equals the stored one bit for bit.
+constexpr float kLog2e = 1.4426950408889634f;
+__device__ __forceinline__ float ex2_approx(float a) {
   float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmaf_rn(x, kAttnLog2e, -m * kAttnLog2e)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(a));
   return y;
 }
-__device__ __forceinline__ double attn_exp(double x, double m) { return exp(x - m); }
+__device__ __forceinline__ float sm_exp(float x, float m) {
+  return ex2_approx(__fmul_rn(__fsub_rn(x, m), kLog2e));
+}
+__device__ __forceinline__ float sm_exp(float hi, float lo, float m) {
+  return ex2_approx(__fmul_rn(__fadd_rn(__fsub_rn(hi, m), lo), kLog2e));
+}
+__device__ __forceinline__ double sm_exp(double x, double m) { return exp(x - m); }
+__device__ __forceinline__ double sm_exp(double hi, double lo, double m) { return exp((hi - m) + lo); }
+
+// u_add_v score a + b as the exact pair hi + lo (TwoSum; order-independent)
+__device__ __forceinline__ void uv_score(float a, float b, float& hi, float& lo) {
+  hi = __fadd_rn(a, b);
+  const float bb = __fsub_rn(hi, a);
+  lo = __fadd_rn(__fsub_rn(a, __fsub_rn(hi, bb)), __fsub_rn(b, bb));
+}
+__device__ __forceinline__ void uv_score(double a, double b, double& hi, double& lo) {
+  hi = __dadd_rn(a, b);
+  const double bb = __dsub_rn(hi, a);
+  lo = __dadd_rn(__dsub_rn(a, __dsub_rn(hi, bb)), __dsub_rn(b, bb));
+}
 
 // attention weight of the edge to/from neighbour nb; same fp operation
 // order as the fused softmax (softmax.cuh: s = el + er; exp(s - max) * inv).
 // MP_AB also returns the neighbour's pack w (the backward's per-destination
-// sum S_v) in w.
+// sum S_v, fp64) in w.
 template <typename T, int MP>
-__device__ __forceinline__ T attn_alpha(const SpmmArgs& a, uint32_t nb, const T (&rc)[3], T& w) {
+__device__ __forceinline__ T attn_alpha(const SpmmArgs& a, uint32_t nb, const T (&rc)[3],
+                                        double& w) {
+  T hi, lo;
   if constexpr (MP == MP_AF) {
-    w = T(0);
-    const T x = __ldg(static_cast<const T*>(a.attn_el) + (uint64_t)nb * a.attn_lde) + rc[0];
-    return attn_exp(x, rc[1]) * rc[2];
+    w = 0.0;
+    uv_score(__ldg(static_cast<const T*>(a.attn_el) + (uint64_t)nb * a.attn_lde), rc[0], hi, lo);
+    return sm_exp(hi, lo, rc[1]) * rc[2];
   } else {
-    T er, mx, inv;
-    load_pack4<T>(static_cast<const T*>(a.attn_pack) + (uint64_t)nb * 4, er, mx, inv, w);
-    const T x = rc[0] + er;
-    return attn_exp(x, mx) * inv;
+    T er, mx, inv, wh;
+    const T* p = static_cast<const T*>(a.attn_pack) + (uint64_t)nb * PackW<T>::value;
+    load_pack4<T>(p, er, mx, inv, wh);
+    w = (double)wh;
+    if constexpr (sizeof(T) == 4) w += (double)__ldg(p + 4);  // same 32 B sector
+    uv_score(rc[0], er, hi, lo);
+    return sm_exp(hi, lo, mx) * inv;
   }
 }
 
@@ -165,9 +221,9 @@ template <typename T, int MP>
 __device__ __forceinline__ T rhs_scalar(const SpmmArgs& a, uint32_t row, const T (&rc)[3],
                                         double& tsum) {
   if constexpr (IsAttn<MP>::value) {
-    T w;
+    double w;
     const T al = attn_alpha<T, MP>(a, row, rc, w);
-    if constexpr (MP == MP_AB) tsum += (double)al * (double)w;
+    if constexpr (MP == MP_AB) tsum += (double)al * w;
     return al;
   } else {
     return __ldg(static_cast<const T*>(a.rhs.data) + (uint64_t)row * a.rhs.ld);
@@ -725,10 +781,27 @@ __device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_
   T* z = static_cast<T*>(a.Z) + row * a.ldz;
   T out[V];
   if constexpr (RHO == RHO_SUM) {
+    int64_t dg = deg;
+    double vs[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) vs[k] = acc.acc[k];
+    if (a.acc64) {
+      double* ap = a.acc64 + row * a.ldacc + col;
+      if (a.acc_mode & kAccRead) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) vs[k] += ap[k];
+      }
+      if (a.acc_mode & kAccStore) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) ap[k] = vs[k];
+      }
+      if (!(a.acc_mode & kAccZ)) return;
+      if (a.deg_full) dg = a.deg_full[row];
+    }
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-      double v = acc.acc[k];
-      if (a.mean && deg > 0) v = v / (double)deg;  // kernels.py:719-722
+      double v = vs[k];
+      if (a.mean && dg > 0) v = v / (double)dg;  // kernels.py:719-722
       out[k] = (T)v;
     }
     if constexpr (V == 4) {

@@ -418,13 +418,33 @@ def _tiled_applies(phi, rho, X, W, d_out, n, tune):
         return False
     F = X.element_size()
     tile = _TILE_BYTES // F
-    if d_out <= tile or n * d_out * F <= _L2_BUDGET:
+    # the gathered slice is X's (source) rows - a row block of a partitioned
+    # graph gathers more (or fewer) rows than it has destinations
+    if d_out <= tile or X.shape[0] * d_out * F <= _L2_BUDGET:
         return False
     aligned = _ld(X) % tile == 0 and X.data_ptr() % 16 == 0
     return not aligned
 
 
-def _gspmm_tiled(g, phi, rho, X, W, Z, d_out):
+def _staged_call(lib, adj, sched, phi, rho, code, lhs, rhs, Z, ldz, d_out, err, tune, stream,
+                 stage, col0=0):
+    """gmp_gspmm, or gmp_gspmm_staged when `stage` = (acc fp64 tensor, mode,
+    deg_full or None) is given (columns col0.. of acc for a column tile)."""
+    if stage is None:
+        return lib.gmp_gspmm(ctypes.byref(_adj_struct(adj)),
+                             ctypes.byref(sched.struct) if sched is not None else None,
+                             _lib.OPS[phi.op], _lib.RHOS[rho], code, _ptr(lhs), _ptr(rhs),
+                             Z, ldz, d_out, None, None, err, _ptr(tune), stream)
+    acc, mode, deg_full = stage
+    return lib.gmp_gspmm_staged(ctypes.byref(_adj_struct(adj)),
+                                ctypes.byref(sched.struct) if sched is not None else None,
+                                _lib.OPS[phi.op], _lib.RHOS[rho], code, _ptr(lhs), _ptr(rhs),
+                                acc.data_ptr() + col0 * 8, _ld(acc), mode,
+                                deg_full.data_ptr() if deg_full is not None else None,
+                                Z, ldz, d_out, err, _ptr(tune), stream)
+
+
+def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None):
     """Aggregation over packed column tiles: gmp_pack_tiles, then one
     gmp_gspmm per 256 B tile (each tile's slice of X stays L2-resident while
     every destination row gathers it; a per-edge scalar is laid out in CSC
@@ -448,33 +468,38 @@ def _gspmm_tiled(g, phi, rho, X, W, Z, d_out):
         rhs = _lib.GmpOperand(_data_ptr(Wc), 1, 1, _lib.TARGETS["edge_pos"])
         if phi.op == "div":
             err = _err_slot(dev)
-    Xp = torch.empty((nt, n, tile), dtype=X.dtype, device=dev)
-    _lib.check(lib.gmp_pack_tiles(n, d_out, code, tile, X.data_ptr(), _ld(X), Xp.data_ptr(),
+    n_src = X.shape[0]  # source rows: packed and gathered; Z has the n destination rows
+    Xp = torch.empty((nt, n_src, tile), dtype=X.dtype, device=dev)
+    _lib.check(lib.gmp_pack_tiles(n_src, d_out, code, tile, X.data_ptr(), _ld(X), Xp.data_ptr(),
                                   stream), "gmp_pack_tiles")
     ldz = _ld(Z)
     for t in range(nt):
         w = min(tile, d_out - t * tile)
         lhs = _lib.GmpOperand(Xp[t].data_ptr(), tile, w, _lib.TARGETS["src"])
-        _lib.check(lib.gmp_gspmm(ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct),
-                                 _lib.OPS[phi.op], _lib.RHOS[rho], code, ctypes.byref(lhs),
-                                 _ptr(rhs), Z.data_ptr() + t * tile * F, ldz, w, None, None,
-                                 err.data_ptr() if err is not None else None, None, stream),
-                   "gmp_gspmm")
+        _lib.check(_staged_call(lib, adj, sched, phi, rho, code, lhs, rhs,
+                                Z.data_ptr() + t * tile * F, ldz, w,
+                                err.data_ptr() if err is not None else None, None, stream,
+                                stage, col0=t * tile), "gmp_gspmm")
     if err is not None:
         pos = int(err.item())
         if pos != _INT32_MAX:
             _raise_div_zero(adj.edge_ids[pos].item())
 
 
-def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None):
+def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None, stage=None):
+    """One g-SpMM launch on g's CSC. `stage` = (acc, mode, deg_full): a staged
+    sum / mean (gmp_gspmm_staged) accumulating into the fp64 buffer acc;
+    Z is written only by the STAGE_LAST launch."""
     lib = _lib.load()
     dev = g.device
     n = g.num_nodes
     ref = next(t for t in (X, Y, W) if t is not None)
+    if stage is not None and (rho not in ("sum", "mean") or phi.op == "dot"):
+        raise ValueError("staged g-SpMM takes sum / mean of non-dot messages")
     if _tiled_applies(phi, rho, X, W, d_out, n, tune):
         Z = out if out is not None else accounting.register(
             torch.empty((n, d_out), dtype=ref.dtype, device=dev))
-        _gspmm_tiled(g, phi, rho, X, W, Z, d_out)
+        _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage)
         return Z, (g.to_csc().degrees().clone() if rho == "mean" else None)
     Z = out if out is not None else accounting.register(
         torch.empty((n, d_out), dtype=ref.dtype, device=dev))
@@ -494,6 +519,17 @@ def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None):
         else:
             rhs = op_w
     sched = adj.schedule() if n > 0 else None
+    if stage is not None:
+        _lib.check(_staged_call(lib, adj, sched, phi, rho, _dtype_code(ref), lhs, rhs,
+                                _data_ptr(Z), _ld(Z) if Z.dim() == 2 and Z.shape[0] else
+                                max(d_out, 1), d_out,
+                                err.data_ptr() if err is not None else None, tune, _stream(dev),
+                                stage), "gmp_gspmm_staged")
+        if err is not None:
+            pos = int(err.item())
+            if pos != _INT32_MAX:
+                _raise_div_zero(adj.edge_ids[pos].item())
+        return Z, None
     st = lib.gmp_gspmm(ctypes.byref(_adj_struct(adj)),
                        ctypes.byref(sched.struct) if sched is not None else None,
                        _lib.OPS[phi.op], _lib.RHOS[rho], _dtype_code(ref),
@@ -600,26 +636,38 @@ def extrema_backward_copy(g, aux, dZ, target, rows):
     out = accounting.register(torch.zeros((rows, d), dtype=dZ.dtype, device=g.device))
     tindex = g.src.data_ptr() if target == "src" else None
     if out.numel():
-        _lib.check(_lib.load().gmp_extrema_bwd_copy(
+        lib = _lib.load()
+        ws = _extrema_workspace(lib, arg.shape[0], d, g.device) if tindex else None
+        _lib.check(lib.gmp_extrema_bwd_copy(
             arg.shape[0], d, _dtype_code(dZ), arg.data_ptr(), dZ.data_ptr(), _ld(dZ), tindex,
-            out.data_ptr(), d, _stream(g.device)), "gmp_extrema_bwd_copy")
+            rows, out.data_ptr(), d, ws.data_ptr() if ws is not None else None,
+            ws.numel() if ws is not None else 0, _stream(g.device)), "gmp_extrema_bwd_copy")
     return out
 
 
-def rowdot(A, B, out, sub=None):
+def _extrema_workspace(lib, n, cells, device):
+    """Scratch of the deterministic many-writer accumulation (sort-grouped
+    fp64 sums) of the fused max/min backward."""
+    return torch.empty(max(1, int(lib.gmp_extrema_bwd_workspace_size(n, cells))),
+                       dtype=torch.uint8, device=device)
+
+
+def rowdot(A, B, out, sub=None, pair=False):
     """out[v] = sum_c A[v,c] B[v,c] - sub[v] in fp64 (gmp_rowdot); out may be a
-    strided column view (e.g. the 4th column of an (n, 4) pack)."""
+    strided column view (e.g. the w column of the attention pack); pair=True
+    stores the fp64 value as hi in out[v] and lo in the next element."""
     n, d = A.shape
-    if B.shape != A.shape or out.shape[0] != n or B.dtype != A.dtype or out.dtype != A.dtype:
-        raise ValueError("rowdot: A, B (n, d) and out (n,) of one dtype")
+    if (B.shape != A.shape or out.shape[0] != n or out.dtype != A.dtype
+            or B.dtype not in (A.dtype, torch.float64)):
+        raise ValueError("rowdot: A, B (n, d) and out (n,) of one dtype (B may be float64)")
     if A.stride(-1) != 1 or B.stride(-1) != 1:
         raise ValueError("rowdot: rows must be contiguous")
     if sub is not None and (sub.dtype != torch.float64 or not sub.is_contiguous()):
         raise ValueError("rowdot: sub must be a contiguous float64 vector")
     _lib.check(_lib.load().gmp_rowdot(
-        n, d, _dtype_code(A), A.data_ptr(), _ld(A) if n > 1 else d, B.data_ptr(),
+        n, d, _dtype_code(A), A.data_ptr(), _ld(A) if n > 1 else d, _dtype_code(B), B.data_ptr(),
         _ld(B) if n > 1 else d, sub.data_ptr() if sub is not None else None, out.data_ptr(),
-        int(out.stride(0)), _stream(A.device)), "gmp_rowdot")
+        int(out.stride(0)), 1 if pair else 0, _stream(A.device)), "gmp_rowdot")
     return out
 
 
@@ -643,10 +691,15 @@ def extrema_backward_binary(g, aux, dZ, phi, role, X, Y, W):
         rhs = _lib.GmpOperand(_data_ptr(mats[phi.rhs_target]), _ld(mats[phi.rhs_target]),
                               mats[phi.rhs_target].shape[1], _lib.TARGETS[phi.rhs_target])
         coo = _lib.GmpCoo(g.num_nodes, g.num_edges, g.src.data_ptr(), g.dst.data_ptr())
-        _lib.check(_lib.load().gmp_extrema_bwd_binary(
+        lib = _lib.load()
+        many = own_t == "src" or (phi.op != "dot" and own_dim == 1)
+        ws = _extrema_workspace(lib, n, own_dim if phi.op == "dot" else d, g.device) \
+            if many else None
+        _lib.check(lib.gmp_extrema_bwd_binary(
             ctypes.byref(coo), n, d, _dtype_code(dZ), arg.data_ptr(), dZ.data_ptr(), _ld(dZ),
             _lib.OPS[phi.op], role, ctypes.byref(lhs), ctypes.byref(rhs), out.data_ptr(),
-            own_dim, own_dim, _stream(g.device)), "gmp_extrema_bwd_binary")
+            own_dim, own_dim, rows, ws.data_ptr() if ws is not None else None,
+            ws.numel() if ws is not None else 0, _stream(g.device)), "gmp_extrema_bwd_binary")
     return out
 
 
@@ -780,13 +833,20 @@ def edge_softmax_uv_stats(g, el, er):
     return stat
 
 
-def gat_aggregate(g, X, el, pack, backward=False):
+def pack_width(dtype):
+    """Elements per 32-byte row of the fused attention's node pack (gmp.h):
+    fp32 [er, max, inv_sum, w_hi, w_lo, 0, 0, 0], fp64 [er, max, inv_sum, w]."""
+    return 4 if dtype == torch.float64 else 8
+
+
+def gat_aggregate(g, X, el, pack, backward=False, z64=None):
     """One head of the fused attention aggregation (gmp_gat_aggregate).
     forward:  Z[v] = sum_{(u,e)->v} alpha_e X[u]   over g's in-adjacency
     backward: Z[u] = sum_{(v,e): u->v} alpha_e X[v] over reverse(g)'s, and
               t[u] = sum_{(v,e): u->v} alpha_e w[v] (fp64); returns (Z, t)
     with alpha_e = exp((el[u] + er[v]) - max[v]) * inv_sum[v] recomputed from
-    el (n, 1) and pack (n, 4) = [er, max, inv_sum, w]."""
+    el (n, 1) and pack (n, pack_width) = [er, max, inv_sum, w (hi, lo)]. z64 (optional (n, d)
+    float64 view) also receives the unrounded rows."""
     from .graph import reverse
     _require_cuda(g)
     X = _as_matrix("X", X, g.num_nodes, g.device)
@@ -797,8 +857,8 @@ def gat_aggregate(g, X, el, pack, backward=False):
         return (Z, t) if backward else Z
     if el.dtype != X.dtype or pack.dtype != X.dtype:
         raise ValueError("el / pack must have the feature dtype")
-    if not (pack.is_contiguous() and pack.shape == (g.num_nodes, 4)):
-        raise ValueError("pack must be a contiguous (n, 4) matrix")
+    if not (pack.is_contiguous() and pack.shape == (g.num_nodes, pack_width(X.dtype))):
+        raise ValueError("pack must be a contiguous (n, %d) matrix" % pack_width(X.dtype))
     walk = reverse(g) if backward else g
     adj = walk.to_csc()
     sched = adj.schedule()
@@ -808,6 +868,8 @@ def gat_aggregate(g, X, el, pack, backward=False):
     _lib.check(_lib.load().gmp_gat_aggregate(
         ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), _dtype_code(X),
         1 if backward else 0, X.data_ptr(), _ld(X), d, el.data_ptr(), lde, pack.data_ptr(),
-        Z.data_ptr(), _ld(Z), t.data_ptr() if backward else None, _ptr(_tuning_struct(None)),
+        Z.data_ptr(), _ld(Z), z64.data_ptr() if z64 is not None else None,
+        _ld(z64) if z64 is not None else 0, t.data_ptr() if backward else None,
+        _ptr(_tuning_struct(None)),
         _stream(g.device)), "gmp_gat_aggregate")
     return (Z, t) if backward else Z

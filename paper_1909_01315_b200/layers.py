@@ -21,6 +21,8 @@ The aggregation runs on the narrower of the input and the projected features
 (linearity: sum alpha (X W) = (sum alpha X) W).
 """
 
+import contextlib
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -57,6 +59,41 @@ def _t(x, device, dtype):
     if torch.is_tensor(x):
         return x
     return torch.as_tensor(np.asarray(x), dtype=dtype, device=device)
+
+
+_dense = threading.local()
+
+
+@contextlib.contextmanager
+def dense_precision(mode):
+    """Precision of the layers' dense products (projections, attention
+    vectors) for fp32 features: "fp32" (default: torch/cuBLAS fp32 GEMMs,
+    TF32 off) or "fp64" (operands up-cast exactly, fp64 products and
+    accumulation, rounded once to fp32 - the same numerics contract as the
+    sparse kernels, so a whole layer matches the reference's float64 layer
+    within north_star's rtol 1e-5 / atol 1e-6; the dense GEMMs are not part
+    of the ported path). Thread-local, like the reference's kernel config
+    (kernels.py:161)."""
+    if mode not in ("fp32", "fp64"):
+        raise ValueError("unknown dense precision %r" % (mode,))
+    prev = getattr(_dense, "mode", "fp32")
+    _dense.mode = mode
+    try:
+        yield
+    finally:
+        _dense.mode = prev
+
+
+def _hi(t):
+    """t in the dense-product precision (fp64 under dense_precision('fp64'))."""
+    if getattr(_dense, "mode", "fp32") == "fp64" and t.dtype == torch.float32:
+        return t.double()
+    return t
+
+
+def _mm(a, b):
+    """a @ b in the dense-product precision, returned in a's dtype."""
+    return (_hi(a) @ _hi(b)).to(a.dtype)
 
 
 def aggregate(g, X, aggregator="mean", **kw):
@@ -104,8 +141,8 @@ def gcn_layer(g, X, params, act="relu", aggregator="mean", order="auto", **kw):
     W = _t(params.W, X.device, X.dtype)
     b = _t(params.b, X.device, X.dtype)
     if _project_first(X, W, order):
-        return _act(aggregate(g, X @ W, aggregator, **kw) + b, act)
-    return _act(aggregate(g, X, aggregator, **kw) @ W + b, act)
+        return _act(aggregate(g, _mm(X, W), aggregator, **kw) + b, act)
+    return _act(_mm(aggregate(g, X, aggregator, **kw), W) + b, act)
 
 
 def sage_layer(g, X, params, act="relu", order="auto", **kw):
@@ -116,8 +153,8 @@ def sage_layer(g, X, params, act="relu", order="auto", **kw):
     Ws = _t(params.W_self, X.device, X.dtype)
     Wn = _t(params.W_neigh, X.device, X.dtype)
     if _project_first(X, Wn, order):
-        return _act(X @ Ws + aggregate(g, X @ Wn, "mean", **kw), act)
-    return _act(X @ Ws + aggregate(g, X, "mean", **kw) @ Wn, act)
+        return _act(_mm(X, Ws) + aggregate(g, _mm(X, Wn), "mean", **kw), act)
+    return _act(_mm(X, Ws) + _mm(aggregate(g, X, "mean", **kw), Wn), act)
 
 
 def gat_layer(g, X, params, num_heads=None, fused=True, **kw):
@@ -141,23 +178,23 @@ def gat_layer(g, X, params, num_heads=None, fused=True, **kw):
     ar = torch.stack([_t(h.a_r, dev, dt)[:, 0] for h in heads])
     # el = proj . a_l = X (W a_l): only (d_in, H) extra weights, no projection needed
     Wv = Wcat.view(d_in, H, D)
-    el = (X @ (Wv * al).sum(-1)).contiguous()                             # (n, H)
-    er = (X @ (Wv * ar).sum(-1)).contiguous()
+    el = _mm(X, (_hi(Wv) * _hi(al)).sum(-1)).contiguous()                # (n, H)
+    er = _mm(X, (_hi(Wv) * _hi(ar)).sum(-1)).contiguous()
     if fused:
         if d_in < D:
             # sum_u alpha_uv (X_u W) = (sum_u alpha_uv X_u) W: aggregate the narrower side
             agg = autodiff.gat_attention(g, el, er, X, shared=True)       # (n, H*d_in)
-            outs = [agg[:, h * d_in:(h + 1) * d_in] @ Wv[:, h, :] for h in range(H)]
+            outs = [_mm(agg[:, h * d_in:(h + 1) * d_in], Wv[:, h, :]) for h in range(H)]
         else:
-            return autodiff.gat_attention(g, el, er, X @ Wcat, shared=False)
+            return autodiff.gat_attention(g, el, er, _mm(X, Wcat), shared=False)
         return outs[0] if H == 1 else torch.cat(outs, dim=1)
     # u_add_v scores + edge_softmax fused: the (m, H) scores are never stored
     alpha = autodiff.edge_softmax_uv(g, el, er)                           # (m, H)
     if d_in < D:
-        outs = [autodiff.gspmm(g, kernels.mul("src", "edge"), "sum", X=X,
-                               W=alpha[:, h:h + 1], **kw) @ Wv[:, h, :] for h in range(H)]
+        outs = [_mm(autodiff.gspmm(g, kernels.mul("src", "edge"), "sum", X=X,
+                                   W=alpha[:, h:h + 1], **kw), Wv[:, h, :]) for h in range(H)]
     else:
-        proj = X @ Wcat                                                   # (n, H*D)
+        proj = _mm(X, Wcat)                                               # (n, H*D)
         outs = [autodiff.gspmm(g, kernels.mul("src", "edge"), "sum",
                                X=proj[:, h * D:(h + 1) * D], W=alpha[:, h:h + 1], **kw)
                 for h in range(H)]

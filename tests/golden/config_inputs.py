@@ -26,3 +26,14 @@ def c2_inputs(seed=1):
     x = rng.random((n, 500), dtype=np.float32)
     u = rng.standard_normal((n, 64)).astype(np.float32)
     return src, dst, n, x, u
+
+
+def c2_weights(init_gat):
+    """C2 head weights: the reference's init_gat(rng 7, 500, 8, 8), rounded to
+    fp32 so the fp32 and fp64 runs and the reference all see the same
+    (exactly representable) values - the fp32 parity protocol."""
+    params = init_gat(np.random.default_rng(7), 500, 8, 8)
+    for hp in params.heads:
+        hp.W, hp.a_l, hp.a_r = (np.asarray(a, np.float32).astype(np.float64)
+                                for a in (hp.W, hp.a_l, hp.a_r))
+    return params

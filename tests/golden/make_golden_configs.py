@@ -9,8 +9,9 @@ sides, so only outputs are stored (tests/golden/configs.npz):
   C1  Cora-shaped (n=2708, m=10556) 2-layer mean-GCN [1433, 16, 7], 20
       epochs of full-graph gradient descent (layers.py:137-202): the losses.
   C2  Pubmed-shaped (n=19717, m=88651) 8-head GAT layer 500 -> 8x8
-      (layers.py:96-116): the output (sampled rows + column sums) and the
-      gradients of sum(h * U) w.r.t. every head's W, a_l, a_r.
+      (layers.py:96-116) with fp32-representable weights: the output (sampled
+      rows + column sums) and the gradients of sum(h * U) w.r.t. every
+      head's W, a_l, a_r.
 """
 
 import sys
@@ -22,7 +23,7 @@ HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from config_inputs import SAMPLE_ROWS, c1_inputs, c2_inputs  # noqa: E402
+from config_inputs import SAMPLE_ROWS, c1_inputs, c2_inputs, c2_weights  # noqa: E402
 
 
 def main():
@@ -40,7 +41,7 @@ def main():
     # ---- C2 ----
     src, dst, n, x, u = c2_inputs()
     g = G.from_arrays(src.astype(np.uint32), dst.astype(np.uint32), num_nodes=n)
-    params = L.init_gat(np.random.default_rng(7), 500, 8, 8)
+    params = c2_weights(L.init_gat)
     tape = G.Tape()
     leaves = []
     heads = []

@@ -92,8 +92,8 @@ def test_round1_entry_points_validate_without_gpu():
     p = ctypes.c_void_p(256)
     adj = _lib.GmpAdj(3, 3, p, p, p)
     # gat aggregate: leading dimension smaller than the width
-    st = lib.gmp_gat_aggregate(ctypes.byref(adj), None, 0, 0, p, 2, 4, p, 1, p, p, 4, None, None,
-                               None)
+    st = lib.gmp_gat_aggregate(ctypes.byref(adj), None, 0, 0, p, 2, 4, p, 1, p, p, 4, None, 0,
+                               None, None, None)
     assert st == _lib.GMP_EINVAL and b"leading" in lib.gmp_last_error()
     # uv stats: null el / er
     st = lib.gmp_edge_softmax_uv_stats(ctypes.byref(adj), None, 0, None, 1, None, 1, 1, p, 64,
@@ -107,15 +107,33 @@ def test_round1_entry_points_validate_without_gpu():
     x = _lib.GmpOperand(p, 4, 4, _lib.TARGETS["src"])
     w = _lib.GmpOperand(p, 1, 1, _lib.TARGETS["edge"])
     st = lib.gmp_extrema_bwd_binary(ctypes.byref(coo), 3, 4, 0, p, p, 4, _lib.OPS["copy_lhs"], 0,
-                                    ctypes.byref(x), ctypes.byref(w), p, 4, 4, None)
+                                    ctypes.byref(x), ctypes.byref(w), p, 4, 4, 3, None, 0, None)
     assert st == _lib.GMP_EINVAL and b"binary extrema backward" in lib.gmp_last_error()
     # dot: d_out must be 1
     st = lib.gmp_extrema_bwd_binary(ctypes.byref(coo), 3, 4, 0, p, p, 4, _lib.OPS["dot"], 0,
-                                    ctypes.byref(x), ctypes.byref(x), p, 4, 4, None)
+                                    ctypes.byref(x), ctypes.byref(x), p, 4, 4, 3, None, 0, None)
     assert st == _lib.GMP_EINVAL and b"d_out must be 1" in lib.gmp_last_error()
     # neighbour sample: negative sizes
     st = lib.gmp_neighbor_sample(p, -1, p, 1, p, 0, p, p, None)
     assert st == _lib.GMP_EINVAL and b"bad sizes" in lib.gmp_last_error()
+    # extrema backward of source rows needs the sort workspace
+    st = lib.gmp_extrema_bwd_copy(3, 4, 0, p, p, 4, p, 3, p, 4, None, 0, None)
+    assert st == _lib.GMP_EINVAL and b"workspace too small" in lib.gmp_last_error()
+    assert lib.gmp_extrema_bwd_workspace_size(0, 4) == 0
+    assert lib.gmp_extrema_bwd_workspace_size(1000, 4) >= 4 * 8 * 4000
+    # staged g-SpMM: reducer, stage mode and accumulator are validated
+    st = lib.gmp_gspmm_staged(ctypes.byref(adj), None, 0, _lib.RHOS["max"], 0, ctypes.byref(x),
+                              None, p, 4, 0, None, p, 4, 4, None, None, None)
+    assert st == _lib.GMP_EINVAL and b"sum / mean" in lib.gmp_last_error()
+    st = lib.gmp_gspmm_staged(ctypes.byref(adj), None, 0, 0, 0, ctypes.byref(x), None, p, 4, 2,
+                              None, p, 4, 4, None, None, None)
+    assert st == _lib.GMP_EINVAL and b"stage mode" in lib.gmp_last_error()
+    st = lib.gmp_gspmm_staged(ctypes.byref(adj), None, 0, 0, 0, ctypes.byref(x), None, None, 4,
+                              0, None, p, 4, 4, None, None, None)
+    assert st == _lib.GMP_EINVAL and b"accumulator" in lib.gmp_last_error()
+    # rowdot: B must be the dtype or f64
+    st = lib.gmp_rowdot(3, 4, 1, p, 4, 0, p, 4, None, p, 1, 0, None)
+    assert st == _lib.GMP_EINVAL and b"B must be" in lib.gmp_last_error()
     # windowed softmax workspace: no schedule -> the plain size
     assert lib.gmp_edge_softmax_workspace_size_ex(ctypes.byref(adj), None, 8, 0, 0) == \
         lib.gmp_edge_softmax_workspace_size(3, 8)

@@ -6,7 +6,7 @@ import torch
 
 import paper_1909_01315_b200 as G
 from paper_1909_01315_b200 import kernels, layers
-from conftest import golden, golden_graph, rel_err, to_np
+from conftest import assert_close32, golden, golden_graph, rel_err, to_np
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -236,8 +236,12 @@ def test_two_process_row_partition_on_gpu():
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_fused_uv_softmax_matches_composition(dtype):
-    """edge_softmax(u_add_v(el, er)) fused == gsddmm(add) then edge_softmax,
-    forward bit-identical (same fp32 score rounding) and gradients equal."""
+    """edge_softmax(u_add_v(el, er)) fused vs gsddmm(add) then edge_softmax.
+    The fused kernels carry the score el + er as an exact pair, so they match
+    the oracle on the exact scores; the composition matches it on the
+    fp32-rounded scores it stores. Both within north_star's fp32 bar, the
+    gradients too."""
+    from oracle import gmp_oracle as O
     s, d = G.generators.power_law_edges(5000, 10, seed=2)
     g = G.from_arrays(s, d, num_nodes=5000, device=DEV)
     for H in (1, 3, 8):
@@ -251,10 +255,18 @@ def test_fused_uv_softmax_matches_composition(dtype):
         score = G.autodiff.gsddmm(g, kernels.add("src", "dst"), X=el, Y=er)
         a2 = G.edge_softmax(g, score)
         (a2 * u).sum().backward()
-        assert torch.equal(a1, a2), H
-        tol = 1e-12 if dtype == torch.float64 else 1e-5
-        assert rel_err(to_np(g1[0]), to_np(el.grad)) < tol
-        assert rel_err(to_np(g1[1]), to_np(er.grad)) < tol
+        exact = to_np(el).astype(np.float64)[s] + to_np(er).astype(np.float64)[d]
+        want1 = O.edge_softmax(s, d, 5000, exact)
+        want2 = O.edge_softmax(s, d, 5000, to_np(score).astype(np.float64))
+        if dtype == torch.float64:
+            assert rel_err(to_np(a1), want1) < 1e-12 and rel_err(to_np(a2), want2) < 1e-12
+            assert rel_err(to_np(g1[0]), to_np(el.grad)) < 1e-12
+            assert rel_err(to_np(g1[1]), to_np(er.grad)) < 1e-12
+        else:
+            assert_close32(a1, want1, "fused alpha H=%d" % H)
+            assert_close32(a2, want2, "composed alpha H=%d" % H)
+            assert_close32(g1[0], to_np(el.grad).astype(np.float64), "d el H=%d" % H)
+            assert_close32(g1[1], to_np(er.grad).astype(np.float64), "d er H=%d" % H)
 
 
 def test_host_pipeline_matches_device_gspmm():
