@@ -234,6 +234,7 @@ class GCNModel:
         self.aggregator = aggregator
         self.order = order
         self.layers = []
+        self.out_dim = dims[-1]
         for a, b in zip(dims, dims[1:]):
             p = init_gcn(rng, a, b)
             self.layers.append(GCNParams(W=_leaf(p.W, device, dtype), b=_leaf(p.b, device, dtype)))
@@ -258,6 +259,7 @@ class SAGEModel:
         device = device or default_device()
         self.order = order
         self.layers = []
+        self.out_dim = dims[-1]
         for a, b in zip(dims, dims[1:]):
             p = init_sage(rng, a, b)
             self.layers.append(SAGEParams(W_self=_leaf(p.W_self, device, dtype),
@@ -285,10 +287,15 @@ class GATModel:
         device = device or default_device()
         self.fused = fused
         self.layers = []
+        self.out_dim = dims[-1]
+        if heads < 1:
+            raise ValueError("head count must be >= 1")
         d_in = dims[0]
         for i, d_out in enumerate(dims[1:]):
             last = i == len(dims) - 2
             h = 1 if last else heads
+            if d_out % h:
+                raise ValueError("hidden width %d is not divisible by %d heads" % (d_out, h))
             p = init_gat(rng, d_in, d_out if last else d_out // h, h)
             for hp in p.heads:
                 hp.W, hp.a_l, hp.a_r = (_leaf(a, device, dtype) for a in (hp.W, hp.a_l, hp.a_r))
@@ -346,7 +353,8 @@ def train(g, features, labels, model, cfg):
         np.asarray(features), dtype=dt, device=dev)
     labels = torch.as_tensor(np.asarray(labels.cpu() if torch.is_tensor(labels) else labels),
                              dtype=torch.int64, device=dev)
-    n_classes = params[-1].shape[1]
+    # the model's output width (GATModel's last parameter is a_r, (D, 1))
+    n_classes = getattr(model, "out_dim", None) or params[-1].shape[1]
     if int(labels.min()) < 0 or int(labels.max()) >= n_classes:
         raise ValueError("label out of range [0, %d)" % n_classes)
     losses = []

@@ -154,86 +154,6 @@ def test_gat_layer_matches_reference(fused):
     assert rel_err(to_np(h), gd["gat/out"]) < 1e-10
 
 
-def test_partition_blocks_sum_to_full_aggregate():
-    """Local-source + remote-source blocks of a rank (the overlapped
-    multi-GPU split) add up to the full row block, which equals the
-    corresponding rows of the single-GPU result; the reverse block gives dX."""
-    from paper_1909_01315_b200 import distributed as D
-    s, d = G.generators.power_law_edges(3000, 12, seed=0)
-    n = 3000
-    g = G.from_arrays(s, d, num_nodes=n, device=DEV)
-    x = torch.randn(n, 24, device=DEV, dtype=torch.float64)
-    full, _ = G.gspmm(g, kernels.copy("src"), "sum", X=x)
-    bounds = D.partition_rows(g.to_csc().indptr, 3)
-    for rank in range(3):
-        pg = D.PartitionedGraph(g.to_csc(), n, rank, 3, bounds=bounds)
-        z_blk = D.local_aggregate(pg.block, x)
-        z_split = D.local_aggregate_offset(pg.local_block, x[pg.r0:pg.r1].contiguous(), pg.r0)
-        z_split += D.local_aggregate(pg.remote_block, x)
-        assert rel_err(to_np(z_blk), to_np(full[pg.r0:pg.r1])) < 1e-12
-        assert rel_err(to_np(z_split), to_np(full[pg.r0:pg.r1])) < 1e-12
-    dz = torch.randn(n, 24, device=DEV, dtype=torch.float64)
-    want = G.gspmm_backward(g, kernels.copy("src"), "sum", X=x, dZ=dz, needs=("x",)).dx
-    got = torch.zeros_like(want)
-    for rank in range(3):
-        pg = D.PartitionedGraph(g.to_csc(), n, rank, 3, bounds=bounds)
-        got += D.local_aggregate(pg.reverse_block(), dz[pg.r0:pg.r1].contiguous())
-    assert rel_err(to_np(got), to_np(want)) < 1e-12
-
-
-def _mp_gpu_worker(rank, world, port, results):
-    import os
-    import torch.distributed as dist
-    from paper_1909_01315_b200 import distributed as D
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    # both ranks share cuda:0; gloo carries the collectives (NCCL refuses
-    # two ranks on one device) while every aggregation runs libgmp kernels
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    s, d = G.generators.power_law_edges(3000, 12, seed=0)
-    n = 3000
-    g = G.from_arrays(s, d, num_nodes=n, device=DEV)
-    pg = D.PartitionedGraph(g.to_csc(), n, rank, world)
-    gen = torch.Generator(device=DEV)
-    gen.manual_seed(0)
-    x = torch.randn((n, 16), generator=gen, device=DEV, dtype=torch.float64)
-    dz = torch.randn((n, 16), generator=gen, device=DEV, dtype=torch.float64)
-    x_local = x[pg.r0:pg.r1].clone().requires_grad_(True)
-    z = D.DistAggregate.apply(x_local, pg, False)
-    (z * dz[pg.r0:pg.r1]).sum().backward()
-    z_ov = pg.aggregate(x[pg.r0:pg.r1].contiguous(), "sum", overlap=True)
-    torch.cuda.synchronize()
-    results[rank] = (pg.r0, pg.r1, z.detach().cpu().numpy(), x_local.grad.cpu().numpy(),
-                     z_ov.cpu().numpy())
-    dist.destroy_process_group()
-
-
-def test_two_process_row_partition_on_gpu():
-    import socket
-    import torch.multiprocessing as mp
-    with socket.socket() as sk:
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-    mgr = mp.Manager()
-    results = mgr.dict()
-    mp.spawn(_mp_gpu_worker, args=(2, port, results), nprocs=2, join=True)
-    s, d = G.generators.power_law_edges(3000, 12, seed=0)
-    n = 3000
-    g = G.from_arrays(s, d, num_nodes=n, device=DEV)
-    gen = torch.Generator(device=DEV)
-    gen.manual_seed(0)
-    x = torch.randn((n, 16), generator=gen, device=DEV, dtype=torch.float64)
-    dz = torch.randn((n, 16), generator=gen, device=DEV, dtype=torch.float64)
-    want, _ = G.gspmm(g, kernels.copy("src"), "sum", X=x)
-    want_dx = G.gspmm_backward(g, kernels.copy("src"), "sum", X=x, dZ=dz, needs=("x",)).dx
-    want, want_dx = to_np(want), to_np(want_dx)
-    for r in range(2):
-        r0, r1, z, dx, z_ov = results[r]
-        assert rel_err(z, want[r0:r1]) < 1e-12
-        assert rel_err(z_ov, want[r0:r1]) < 1e-12
-        assert rel_err(dx, want_dx[r0:r1]) < 1e-12
-
-
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_fused_uv_softmax_matches_composition(dtype):
     """edge_softmax(u_add_v(el, er)) fused vs gsddmm(add) then edge_softmax.

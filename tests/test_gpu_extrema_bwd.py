@@ -67,3 +67,47 @@ def test_fused_binary_extrema_logs_no_dense_route():
         G.gspmm_backward(g, kernels.mul("src", "edge"), "max", X=X, W=W, aux=aux,
                          dZ=torch.ones_like(z), needs=("x", "w"))
     assert [r.phi for r in log] == ["argext_grad(mul(src,edge),0)", "argext_grad(mul(src,edge),1)"]
+
+
+@pytest.mark.parametrize("op", ["copy", "mul", "dot", "add"])
+def test_many_writer_gradients_deterministic_fp64(op):
+    """Source rows (and broadcast operands) that win several cells are summed
+    in fp64, in a fixed order, and rounded once (sort-grouped, no float
+    atomics): fp32 gradients equal the oracle's fp64 sums rounded to fp32 to
+    north_star's bar and are bit-identical run to run."""
+    from oracle import gmp_oracle as O
+    from conftest import assert_close32
+    s, d = G.generators.power_law_edges(6000, 12, seed=7)
+    n, m = 6000, s.size
+    g = G.from_arrays(s, d, num_nodes=n, device=DEV)
+    rng = np.random.default_rng(3)
+    dd = 5
+    X = rng.standard_normal((n, dd)).astype(np.float32)
+    if op == "copy":
+        phi, name, kw, okw = kernels.copy("src"), "copy_lhs", {}, {}
+    elif op == "dot":
+        Y = rng.standard_normal((n, dd)).astype(np.float32)
+        phi, name = kernels.dot("src", "dst"), "dot"
+        kw, okw = {"Y": torch.as_tensor(Y, device=DEV)}, {"Y": Y}
+    else:
+        W = rng.standard_normal((m, 1)).astype(np.float32)   # broadcast edge operand
+        phi, name = kernels.MessageFunc(op, "src", "edge"), op
+        kw, okw = {"W": torch.as_tensor(W, device=DEV)}, {"W": W}
+    Xt = torch.as_tensor(X, device=DEV)
+    z, aux = G.gspmm(g, phi, "max", X=Xt, **kw)
+    dz = torch.as_tensor(rng.standard_normal(tuple(z.shape)).astype(np.float32), device=DEV)
+    needs = ("x",) + tuple(k.lower() for k in kw)
+    runs = [G.gspmm_backward(g, phi, "max", X=Xt, **kw, aux=aux, dZ=dz, needs=needs)
+            for _ in range(3)]
+    rt = None if op == "copy" else ("dst" if op == "dot" else "edge")
+    want = O.gspmm_backward(s, d, n, name, "src", rt, "max",
+                            X=X.astype(np.float64),
+                            **{k: v.astype(np.float64) for k, v in okw.items()},
+                            aux=to_np(aux.arg_edge), dZ=to_np(dz).astype(np.float64))
+    for attr, key in (("dx", "src"), ("dy", "dst"), ("dw", "edge")):
+        got = getattr(runs[0], attr, None)
+        if got is None or key not in want:
+            continue
+        assert_close32(got, want[key], "%s %s" % (op, attr))
+        for r in runs[1:]:
+            assert torch.equal(getattr(r, attr), got), (op, attr)

@@ -273,3 +273,37 @@ def test_layer_order_validation():
     assert not layers._project_first(None, W, "aggregate_first")
     with pytest.raises(ValueError):
         layers._project_first(None, W, "sideways")
+
+
+def test_tiled_path_sized_by_source_rows():
+    """A row block of a partitioned graph gathers more source rows than it
+    has destination rows: the L2 test and the packing use X's rows (ADVICE
+    r1: the tiles were packed with the destination count)."""
+    from paper_1909_01315_b200.kernels import _tiled_applies
+    cp = kernels.copy("src")
+    X = torch.empty((232965, 602))
+    assert _tiled_applies(cp, "sum", X, None, 602, 2000, None)     # few destination rows
+    assert not _tiled_applies(cp, "sum", torch.empty((2000, 602)), None, 602, 232965, None)
+
+
+def test_models_know_their_output_width():
+    from paper_1909_01315_b200 import layers
+    m = layers.GATModel([12, 8, 8, 5], heads=2, seed=0, device="cpu")
+    assert m.out_dim == 5
+    assert layers.GCNModel([12, 8, 3], seed=0, device="cpu").out_dim == 3
+    with pytest.raises(ValueError, match="divisible"):
+        layers.GATModel([12, 9, 5], heads=2, seed=0, device="cpu")
+
+
+def test_dense_precision_context():
+    from paper_1909_01315_b200 import layers
+    a = torch.randn(5, 7)
+    b = torch.randn(7, 3)
+    with layers.dense_precision("fp64"):
+        got = layers._mm(a, b)
+    assert got.dtype == torch.float32
+    assert torch.equal(got, (a.double() @ b.double()).float())
+    assert torch.equal(layers._mm(a, b), a @ b)
+    with pytest.raises(ValueError):
+        with layers.dense_precision("fp16"):
+            pass
