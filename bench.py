@@ -3,20 +3,40 @@
 Workload (config C3, BASELINE.json configs[2]): the reference's own
 power_law(232965, 492, seed=0) graph (m = 114,497,502), X ~ N(0,1) fp32 with
 d = 602, one copy_u + sum g-SpMM per step (the first GCN layer's
-aggregation). value = algorithmic bytes / kernel time with inputs resident in
+aggregation). value = algorithmic bytes / step time with inputs resident in
 HBM, bytes = (n+1)*8 + m*4 + m*d*4 + n*d*4. L2 is flushed
 (256 MiB write) between timed steps, outside the timed events.
 
-e2e: the same op through the public API (paper_1909_01315_b200.gspmm) with
-X copied from pinned host memory before and Z copied back after, every step.
-Extras: other ops of the sweep, fused edge_softmax, GCN / SAGE epoch ms.
+roofline: the dominant kernel is the row kernel over one packed 256 B column
+tile; its gathers are served from L2 (the tile slice of X is L2-resident), so
+the bound is the L2 gather bandwidth, measured live in this run by
+gmp_probe_l2_gather (random 256 B rows from a slice of the same size, same
+count); achieved = m * 256 B gathered per tile launch / the launch's mean
+duration (CUDA events around each launch). The no-reuse HBM byte model is
+kept under roofline.hbm_model.
+
+e2e: the same op through the public API (pipeline.gspmm_host) with X copied
+from pinned host memory and Z copied back inside the timed region.
+Extras: other ops of the sweep, fused edge_softmax, GCN / SAGE / GAT epochs.
+
+Parity gate (the reference's own bench refuses to time an incorrect kernel,
+/root/reference/pkg/src/graphmp/bench.py:116-141): the headline and every
+extra op are compared on a bounded sample (strided destination rows with all
+their in-edges; strided edge ids for g-SDDMM) against the reference itself
+(graphmp from baseline/_ref, kind "reference"; the oracle port if it is not
+installed, kind "port"): max/min values and arg edges bit-exact, sums /
+softmax within rtol 1e-5 / atol 1e-6. A mismatch prints the line with
+parity.ok = false and exits 2. The same reference calls are timed on all host
+cores: cpu_baseline (headline) and extras.*.cpu.
 
 N > 1 (torchrun): destination rows partitioned by equal edge counts; every
-step all-gathers the row-sharded X over NCCL and runs the local rows
-(strong scaling: the whole graph is fixed). Timing is max over ranks.
+step runs the row-partitioned aggregation (local shard first, remote shards
+as they land, distributed.PartitionedGraph) - strong scaling, max over ranks
+- plus a row-partitioned GCN epoch (DistGCN) and the shard exchange alone
+(NVLink fraction).
 
---impl reference: the CPU oracle port of the reference (oracle/gmp_oracle.py,
-node_parallel restatement) on a bounded row sample, all host threads.
+--impl reference: the reference's node_parallel g-SpMM (graphmp, all host
+threads) on the same row sample as cpu_baseline, per step.
 """
 
 import argparse
@@ -34,6 +54,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 N_NODES, AVG_DEG, FEAT, HIDDEN, CLASSES = 232_965, 492, 602, 16, 41
+RTOL, ATOL = 1e-5, 1e-6
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU
 
 
 def parse():
@@ -46,9 +68,10 @@ def parse():
     p.add_argument("--deg", type=int, default=AVG_DEG)
     p.add_argument("--feat", type=int, default=FEAT)
     p.add_argument("--no-extras", action="store_true")
-    p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-edges", type=int, default=24_000_000,
-                   help="edges in the CPU baseline sample (strided rows)")
+    p.add_argument("--no-cpu", action="store_true",
+                   help="skip the CPU leg (no parity gate, no cpu_baseline)")
+    p.add_argument("--cpu-edges", type=int, default=6_000_000,
+                   help="edges in the headline CPU / parity sample (strided rows)")
     p.add_argument("--tile-cols", type=int, default=0)
     p.add_argument("--workload", default="reddit", choices=["reddit", "rmat"],
                    help="reddit: config C3 (default); rmat: config C4, 10M nodes / 1B edges / d=256")
@@ -137,71 +160,198 @@ def build_graph_arrays(args):
     return s, d, time.time() - t0
 
 
-# ----------------------------------------------------------------- CPU leg ---
-
-def strided_rows(indptr, n_edges_target):
-    """Every k-th destination row of the CSC, k chosen so the sample holds
-    ~n_edges_target edges: a cross-section of the whole degree distribution
-    (hubs and the long tail), not a prefix of hub rows."""
-    n = indptr.size - 1
-    m = int(indptr[-1])
-    k = max(1, int(round(m / max(1, n_edges_target))))
-    return np.arange(0, n, k, dtype=np.int64)
-
-
-def sub_csc(indptr, indices, eids, rows):
-    lens = (indptr[rows + 1] - indptr[rows]).astype(np.int64)
-    sub_ptr = np.zeros(rows.size + 1, dtype=np.int64)
-    np.cumsum(lens, out=sub_ptr[1:])
-    pos = np.repeat(indptr[rows] - sub_ptr[:-1], lens) + np.arange(int(sub_ptr[-1]), dtype=np.int64)
-    return sub_ptr, indices[pos], eids[pos]
-
-
-def cpu_sample(indptr, indices, eids, x, n_edges_target, workers):
-    """Time the oracle's node_parallel g-SpMM (the reference algorithm,
-    kernels.py:473-482) on a strided sample of destination rows holding
-    ~n_edges_target edges. Returns (seconds, algorithmic bytes, rows, edges)."""
-    from oracle import gmp_oracle as O
-    rows = strided_rows(indptr, n_edges_target)
-    sub_ptr, sub_ind, sub_eid = sub_csc(indptr, indices, eids, rows)
-    # only the source rows the sample touches are handed to the CPU (the
-    # gathers read the same values; keeps host memory bounded on 1B edges)
-    used, remap = np.unique(sub_ind, return_inverse=True)
-    x = np.asarray(x[used], dtype=np.float64)
-    sub = (sub_ptr, remap.astype(np.int64), sub_eid)
-    r, e = rows.size, int(sub_ptr[-1])
-    d = x.shape[1]
-    t0 = time.perf_counter()
-    O.gspmm(None, None, r, "copy_lhs", "src", None, "sum", X=x, workers=workers, adj=sub)
-    dt = time.perf_counter() - t0
-    return dt, spmm_bytes(r, e, d), r, e
-
-
-def run_reference(args):
-    """--impl reference: the CPU port of the reference's node_parallel g-SpMM."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from oracle import gmp_oracle as O
-    s, d, gen_s = build_graph_arrays(args)
-    n, m = args.nodes, s.size
-    # CSC with the reference's ordering (graph.py:35-44), built by one stable
-    # argsort of dst * n + src (equivalent to its lexsort; not timed)
+def host_csc(s, d, n):
+    """CSC with the reference's ordering (graph.py:35-44): one stable argsort
+    of dst * n + src (equivalent to its lexsort; not timed)."""
     order = np.argsort(d.astype(np.int64) * n + s, kind="stable")
     indptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(np.bincount(d, minlength=n), out=indptr[1:])
-    indices, eids = s[order], order
+    return indptr, s[order].astype(np.int64), order.astype(np.int64)
+
+
+# ------------------------------------------------------- the reference (CPU) ---
+
+def load_reference():
+    """graphmp (the unmodified reference) from baseline/_ref -> (module,
+    "reference"); the oracle port (oracle/gmp_oracle.py) when it is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if ref.exists():
+        sys.path.insert(0, str(ref))
+        try:
+            import graphmp
+            return graphmp, "reference"
+        except Exception:
+            pass
+    from oracle import gmp_oracle
+    return gmp_oracle, "port"
+
+
+class RowSample:
+    """Every k-th destination row of the CSC (k chosen for ~target edges: a
+    cross-section of the degree distribution, hubs and tail) with all its
+    in-edges, as a standalone graph: edges in global edge-id order (so the
+    reference's smallest-edge-id tie-break is the same), sources remapped to
+    0..U-1, row i of the sample = destination rows[i]."""
+
+    def __init__(self, indptr, indices, eids, target_edges):
+        n = indptr.size - 1
+        m = int(indptr[-1])
+        k = max(1, int(round(m / max(1, target_edges))))
+        self.rows = np.arange(0, n, k, dtype=np.int64)
+        lens = (indptr[self.rows + 1] - indptr[self.rows]).astype(np.int64)
+        ptr = np.zeros(self.rows.size + 1, dtype=np.int64)
+        np.cumsum(lens, out=ptr[1:])
+        pos = np.repeat(indptr[self.rows] - ptr[:-1], lens) + np.arange(int(ptr[-1]))
+        local_row = np.repeat(np.arange(self.rows.size), lens)
+        order = np.argsort(eids[pos], kind="stable")
+        self.geid = eids[pos][order]                 # global edge id of sample edge j
+        self.used, src = np.unique(indices[pos][order], return_inverse=True)
+        self.src = src.astype(np.int64)
+        self.dst = local_row[order].astype(np.int64)
+        self.n = max(self.used.size, self.rows.size)
+        self.m = self.geid.size
+
+    def describe(self):
+        return "%d destination rows (every k-th CSC row) / %d edges" % (self.rows.size, self.m)
+
+    def pad(self, x_used):
+        """Source rows padded to the sample's node count (the reference wants
+        one feature row per node)."""
+        out = np.zeros((self.n, x_used.shape[1]), dtype=np.float64)
+        out[:x_used.shape[0]] = x_used
+        return out
+
+
+class EdgeSample:
+    """Every k-th edge id, as a graph over the union of their endpoints."""
+
+    def __init__(self, s, d, target_edges):
+        m = s.size
+        k = max(1, int(round(m / max(1, target_edges))))
+        self.geid = np.arange(0, m, k, dtype=np.int64)
+        nodes, inv = np.unique(np.concatenate([s[self.geid], d[self.geid]]),
+                               return_inverse=True)
+        self.nodes = nodes
+        self.src = inv[:self.geid.size].astype(np.int64)
+        self.dst = inv[self.geid.size:].astype(np.int64)
+        self.n = nodes.size
+        self.m = self.geid.size
+
+    def describe(self):
+        return "every k-th edge id: %d edges" % self.m
+
+
+class RefCPU:
+    """The reference's default strategies (node_parallel g-SpMM, edge_parallel
+    g-SDDMM, kernels.py:473-482,829-836) on all host cores; every call timed
+    (graph indices built before the clock starts)."""
+
+    def __init__(self):
+        self.mod, self.kind = load_reference()
+        self.cores = len(os.sched_getaffinity(0))
+
+    def _graph(self, src, dst, n):
+        G = self.mod
+        g = G.from_arrays(src.astype(np.uint32), dst.astype(np.uint32), num_nodes=n)
+        g.to_csc()
+        return g
+
+    def gspmm(self, smp, op, rho, X, W=None):
+        """-> (Z rows of the sample, arg as global edge ids or None, seconds)."""
+        if self.kind == "port":
+            O = self.mod
+            adj = (np.concatenate([[0], np.cumsum(np.bincount(smp.dst, minlength=smp.n))]),
+                   None, None)
+            order = np.argsort(smp.dst * smp.n + smp.src, kind="stable")
+            adj = (adj[0], smp.src[order], order)
+            t0 = time.perf_counter()
+            z, arg = O.gspmm(None, None, smp.n, op, "src", "edge" if W is not None else None,
+                             rho, X=X, W=W, workers=self.cores, adj=adj)
+            dt = time.perf_counter() - t0
+        else:
+            G = self.mod
+            K = G.kernels
+            g = self._graph(smp.src, smp.dst, smp.n)
+            phi = K.copy("src") if op == "copy_lhs" else K.MessageFunc(op, "src", "edge")
+            with K.default_workers(self.cores):
+                t0 = time.perf_counter()
+                z, aux = G.gspmm(g, phi, rho, X=X, W=W)
+                dt = time.perf_counter() - t0
+            arg = aux.arg_edge if rho in ("max", "min") else None
+        z = z[:smp.rows.size]
+        if arg is not None:
+            arg = arg[:smp.rows.size]
+            arg = np.where(arg >= 0, smp.geid[np.maximum(arg, 0)], -1)
+        return z, arg, dt
+
+    def gsddmm_dot(self, smp, X):
+        if self.kind == "port":
+            t0 = time.perf_counter()
+            mm = self.mod.gsddmm(smp.src, smp.dst, smp.n, "dot", "src", "dst", X=X, Y=X,
+                                 workers=self.cores)
+            return mm, time.perf_counter() - t0
+        G = self.mod
+        g = G.from_arrays(smp.src.astype(np.uint32), smp.dst.astype(np.uint32), num_nodes=smp.n)
+        with G.kernels.default_workers(self.cores):
+            t0 = time.perf_counter()
+            mm = G.gsddmm(g, G.kernels.dot("src", "dst"), X=X, Y=X)
+            return mm, time.perf_counter() - t0
+
+    def edge_softmax(self, smp, scores):
+        if self.kind == "port":
+            t0 = time.perf_counter()
+            a = self.mod.edge_softmax(smp.src, smp.dst, smp.n, scores)
+            return a, time.perf_counter() - t0
+        G = self.mod
+        g = self._graph(smp.src, smp.dst, smp.n)
+        with G.kernels.default_workers(self.cores):
+            t0 = time.perf_counter()
+            a = G.edge_softmax(g, scores)
+            return np.asarray(a), time.perf_counter() - t0
+
+
+def compare(got, want, exact=False):
+    """Parity record: bit-exact (IEEE equality, -0 == +0 as np.array_equal)
+    or elementwise rtol 1e-5 / atol 1e-6."""
+    got = np.asarray(got)
+    want = np.asarray(want)
+    if exact:
+        ok = got == want.astype(got.dtype)
+    else:
+        ok = np.isclose(got.astype(np.float64), want.astype(np.float64), rtol=RTOL, atol=ATOL)
+    diff = np.abs(got.astype(np.float64) - want.astype(np.float64))
+    return {"ok": bool(ok.all()), "cells": int(ok.size), "bad": int((~ok).sum()),
+            "max_abs": float(diff.max()) if diff.size else 0.0,
+            "bar": "bit-exact" if exact else "rtol 1e-5 / atol 1e-6"}
+
+
+def merge(*recs):
+    out = {"ok": all(r["ok"] for r in recs), "cells": sum(r["cells"] for r in recs),
+           "bad": sum(r["bad"] for r in recs), "max_abs": max(r["max_abs"] for r in recs),
+           "bar": " + ".join(sorted({r["bar"] for r in recs}))}
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the reference's node_parallel g-SpMM (copy_u + sum)
+    on the headline row sample, every step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    s, d, gen_s = build_graph_arrays(args)
+    n, m = args.nodes, s.size
+    indptr, indices, eids = host_csc(s, d, n)
+    smp = RowSample(indptr, indices, eids, args.cpu_edges)
     rng = np.random.default_rng(0)
-    x = rng.standard_normal((n, args.feat), dtype=np.float32).astype(np.float64)
-    workers = len(os.sched_getaffinity(0))
-    sample_edges = min(args.cpu_edges // 4, m)
+    x = smp.pad(rng.standard_normal((smp.used.size, args.feat), dtype=np.float32)
+                .astype(np.float64))
+    ref = RefCPU()
     for _ in range(args.warmup):
-        cpu_sample(indptr, indices, eids, x, max(1, sample_edges // 20), workers)
-    secs, nbytes = 0.0, 0
+        ref.gspmm(smp, "copy_lhs", "sum", x)
+    secs = 0.0
     for _ in range(args.steps):
-        dt, b, r, e = cpu_sample(indptr, indices, eids, x, sample_edges, workers)
-        secs += dt
-        nbytes += b
+        secs += ref.gspmm(smp, "copy_lhs", "sum", x)[2]
+    nbytes = spmm_bytes(smp.rows.size, smp.m, args.feat) * args.steps
     gbs = nbytes / secs / 1e9
     line = {
         "impl": "reference", "metric": "g-SpMM achieved GB/s (copy_u+sum, Reddit-shaped, d=%d)" % args.feat,
@@ -210,10 +360,12 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference power_law(%d, %d, seed=0) graph, X~N(0,1)" % (n, args.deg),
         "config": {"workload": "reddit_spmm_copy_u_sum", "nodes": n, "edges": int(m),
-                   "feat": args.feat, "sample_rows": r, "sample_edges": e},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": workers, "kind": "port",
-                         "sample": "every k-th CSC row: %d rows / %d edges of the Reddit-shaped "
-                                   "graph per step, d=%d" % (r, e, args.feat)},
+                   "feat": args.feat, "sample_rows": int(smp.rows.size),
+                   "sample_edges": int(smp.m)},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": ref.cores,
+                         "kind": ref.kind,
+                         "sample": smp.describe() + " of the Reddit-shaped graph per step, d=%d, "
+                                   "graphmp node_parallel, %d workers" % (args.feat, ref.cores)},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -231,7 +383,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1909_01315_b200 as G
-    from paper_1909_01315_b200 import _lib, distributed, kernels, layers
+    from paper_1909_01315_b200 import _lib, distributed, kernels
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -248,6 +400,7 @@ def main():
             dist.init_process_group(backend)
     torch.backends.cuda.matmul.allow_tf32 = False
 
+    s = d = None
     if args.workload == "rmat":
         t0 = time.time()
         g = G.rmat(args.nodes, args.edges, seed=0, device=dev)
@@ -273,22 +426,20 @@ def main():
         tune = kernels.tuning(tile_cols=args.tile_cols)
         tune.__enter__()
 
+    pg = None
     if world > 1:
         pg = distributed.PartitionedGraph(adj, n, rank, world)
         x_local = X[pg.r0:pg.r1].contiguous()
-        for blk in (pg.block, pg.local_block, pg.remote_block):
-            blk.to_csc().schedule()
 
         def step():
             return pg.aggregate(x_local, "sum", overlap=True)
-        step_bytes = spmm_bytes(n, m, F)
     else:
         def step():
             return G.gspmm(g, phi, "sum", X=X)[0]
-        step_bytes = spmm_bytes(n, m, F)
+    step_bytes = spmm_bytes(n, m, F)
 
     for _ in range(max(3, args.warmup)):
-        step()
+        z_last = step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -300,7 +451,7 @@ def main():
             flush.fill_(1)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            step()
+            z_last = step()
             b.record(stream)
             b.synchronize()
             times.append(a.elapsed_time(b))
@@ -314,6 +465,11 @@ def main():
         dist.barrier()
     value = step_bytes / (ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
+
+    roofline = None
+    if world == 1:
+        roofline = kernel_roofline(torch, kernels, _lib, g, X, n, m, F, value, ms, peak,
+                                   peak_kind, step_bytes, stream, flush)
 
     # e2e through the public API with host buffers: pipeline.gspmm_host takes
     # pinned host X and returns host Z, H2D / kernel / D2H overlapped per tile
@@ -338,45 +494,34 @@ def main():
                "d2h_bytes_per_step": int(zh.numel() * 4),
                "api": "paper_1909_01315_b200.pipeline.gspmm_host (pinned host X -> host Z, "
                       "copies overlapped with the kernel per column tile)"}
-        zref = G.gspmm(g, phi, "sum", X=X)[0].cpu()
-        e2e["matches_device_result"] = bool(torch.equal(zref, zh))
+        e2e["matches_device_result"] = bool(torch.equal(z_last.cpu(), zh))
+        del xh, zh
 
-    extras = {}
+    extras, outs = {}, {}
     if rank == 0 and world == 1 and not args.no_extras:
-        extras = run_extras(G, kernels, layers, g, X, n, m, flush, stream, dev, args)
+        extras, outs = run_extras(G, kernels, g, X, n, m, flush, stream, dev)
+    multi = None
+    if world > 1:
+        multi = run_multi(torch, dist, distributed, pg, X, n, F, flush, stream, dev, rank)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        indptr, indices, eids = adj.numpy()
-        workers = len(os.sched_getaffinity(0))
-        xc = X.cpu().numpy()
-        dt, nb, r, e = cpu_sample(indptr, indices.astype(np.int64), eids.astype(np.int64), xc,
-                                  args.cpu_edges, workers)
-        cpu = {"value": round(nb / dt / 1e9, 3), "unit": "GB/s", "cores": workers, "kind": "port",
-               "seconds": round(dt, 2),
-               "sample": "oracle node_parallel copy_u+sum on every k-th CSC row: %d rows / %d "
-                         "edges, d=%d, %d threads" % (r, e, F, workers)}
+    # CPU leg: the reference on bounded samples - parity gate + CPU timings
+    cpu, parity = None, None
+    if rank == 0 and world == 1 and not args.no_cpu and s is not None:
+        cpu, parity = cpu_leg(torch, args, s, d, adj, X, z_last, outs, extras, n, m, F)
 
     traffic = None
-    l2 = None
     tpath = ROOT / "profiles" / "ncu_traffic.json"
-    if tpath.exists():
+    if tpath.exists() and roofline is not None:
         try:
             tj = json.loads(tpath.read_text())
             if tj.get("feat") == F and tj.get("edges") == m:
-                traffic = tj.get("dram_bytes_per_launch")
-                l2b = tj.get("row_kernel_l2_read_bytes")
-                cpath = ROOT / "profiles" / "l2_gather_ceiling.json"
-                if l2b and cpath.exists():
-                    ceil = float(json.loads(cpath.read_text())["ceiling_gbs_60mb"])
-                    ach = l2b / (ms * 1e-3) / 1e9
-                    l2 = {"read_bytes_per_step": l2b, "achieved_gbs": round(ach, 1),
-                          "gather_ceiling_gbs": ceil, "frac": round(ach / ceil, 4),
-                          "source": "profiles/ncu_traffic.json (ncu L2 sectors of the row "
-                                    "kernel launches) over this run's step time; ceiling "
-                                    "profiles/l2_gather_ceiling.json"}
+                traffic = tj.get("row_kernel_dram_bytes_per_launch") or None
+                roofline["traffic_source"] = "profiles/ncu_traffic.json (ncu --set full, " \
+                                             "dram__bytes_read+write of one tile launch)"
         except Exception:
             traffic = None
+    if roofline is not None:
+        roofline["traffic"] = traffic
 
     if rank == 0:
         sched = adj.schedule()
@@ -395,53 +540,112 @@ def main():
                        "l2": "flushed between steps (256 MiB write, outside timed events)",
                        "parallelism": "row-partition x%d" % world if world > 1 else "single GPU",
                        "graph_gen_s": round(gen_s, 1), "csc_build_s": round(build_s, 2)},
-            "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(value / peak, 4), "traffic": traffic,
-                         "peak_kind": peak_kind,
-                         "kernel": "spmm_rows_kernel<float,COPY,SUM> over packed 256 B column tiles",
-                         "bytes_per_launch": step_bytes,
-                         "note": "achieved = algorithmic (no-reuse) bytes per step / step time; "
-                                 "frac > 1 because each column tile of X is L2-resident while "
-                                 "every row gathers it - traffic is the measured DRAM bytes and "
-                                 "l2 the bound that binds",
-                         "l2": l2},
+            "roofline": roofline,
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "clocks": clocks.summary(),
             "gpu_launches": int(launches),
             "extras": extras,
         }
+        if multi is not None:
+            line["multi_gpu"] = multi
         print(json.dumps(line), flush=True)
     if tune is not None:
         tune.__exit__(None, None, None)
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        print("PARITY FAILURE: the GPU result differs from the reference (see parity)",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
+
+
+def kernel_roofline(torch, kernels, _lib, g, X, n, m, F, value, ms, peak, peak_kind,
+                    step_bytes, stream, flush):
+    """The dominant kernel (one packed-tile row-kernel launch) against the L2
+    gather ceiling measured live; the no-reuse HBM model beside it."""
+    rf = {"bound": "l2", "unit": "GB/s"}
+    phi = kernels.copy("src")
+    if not kernels._tiled_applies(phi, "sum", X, None, F, n, kernels._tuning_struct(None)):
+        rf["note"] = "workload not on the packed-tile path"
+        rf.update({"bound": "hbm", "achieved": round(value, 1), "peak": peak,
+                   "frac": round(value / peak, 4)})
+        return rf
+    Z = torch.empty((n, F), dtype=X.dtype, device=X.device)
+    per = []
+    for _ in range(3):
+        flush.fill_(1)
+        ev = []
+        kernels._gspmm_tiled(g, phi, "sum", X, None, Z, F, events=ev)
+        torch.cuda.synchronize()
+        per.extend(a.elapsed_time(b) for a, b in ev)
+    t_tile = float(np.mean(per))
+    ntiles = len(ev)
+    # the live ceiling: m random 256 B rows from an n x 256 B slice (one tile)
+    lib = _lib.load()
+    slice_ = torch.zeros((n, 64), dtype=torch.float32, device=X.device)
+    sink = torch.zeros(1, dtype=torch.float32, device=X.device)
+    st = kernels._stream(X.device)
+    pt = []
+    for i in range(4):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _lib.check(lib.gmp_probe_l2_gather(slice_.data_ptr(), n, 256, m, sink.data_ptr(), st),
+                   "gmp_probe_l2_gather")
+        b.record(stream)
+        b.synchronize()
+        if i:
+            pt.append(a.elapsed_time(b))
+    t_probe = float(np.min(pt))
+    gathered = m * 256
+    ceiling = gathered / (t_probe * 1e-3) / 1e9
+    achieved = gathered / (t_tile * 1e-3) / 1e9
+    rf.update({
+        "achieved": round(achieved, 1), "peak": round(ceiling, 1), "frac": round(achieved / ceiling, 4),
+        "peak_kind": "measured live: gmp_probe_l2_gather, %d random 256 B rows from a %.1f MB "
+                     "slice (best of 3)" % (m, n * 256 / 2 ** 20),
+        "kernel": "spmm_rows_kernel<float,COPY,SUM,V=4,MP_F> over one packed 256 B column tile",
+        "bytes_per_launch": gathered,
+        "bytes_model": "m x 256 B: one 256 B packed tile row gathered per edge (whole sectors)",
+        "launch_ms": round(t_tile, 4), "launches_per_step": ntiles,
+        "share_of_step": round(t_tile * ntiles / ms, 4),
+        "hbm_model": {"achieved": round(value, 1), "peak": peak, "peak_kind": peak_kind,
+                      "frac": round(value / peak, 4), "bytes_per_step": step_bytes,
+                      "note": "no-reuse algorithmic bytes (SURVEY 8(d)) / step time: > 1 "
+                              "because every gather after a tile's first touch hits L2"},
+    })
+    del slice_, Z
+    return rf
 
 
 def _time(fn, stream, flush, reps=5):
     import torch
-    fn()
+    out = fn()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         flush.fill_(1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        fn()
+        out = fn()
         b.record(stream)
         b.synchronize()
         ts.append(a.elapsed_time(b))
-    return float(np.median(ts))
+    return float(np.median(ts)), out
 
 
-def run_extras(G, kernels, layers, g, X, n, m, flush, stream, dev, args):
+def run_extras(G, kernels, g, X, n, m, flush, stream, dev):
     import torch
-    out = {}
+    from paper_1909_01315_b200 import layers
+    out, keep = {}, {}
     gen = torch.Generator(device=dev)
     gen.manual_seed(1)
     F = X.shape[1]
     w1 = torch.randn((m, 1), generator=gen, device=dev)
     x16 = torch.randn((n, 16), generator=gen, device=dev)
+    s8 = torch.randn((m, 8), generator=gen, device=dev)
+    keep.update(w1=w1, x16=x16, s8=s8)
     cases = [
         ("copy_u_sum_d16", lambda: G.gspmm(g, kernels.copy("src"), "sum", X=x16),
          spmm_bytes(n, m, 16)),
@@ -451,27 +655,143 @@ def run_extras(G, kernels, layers, g, X, n, m, flush, stream, dev, args):
          spmm_bytes(n, m, F) + m * 4 + m * 4),
         ("u_dot_v_d16", lambda: G.gsddmm(g, kernels.dot("src", "dst"), X=x16, Y=x16),
          2 * m * 4 + 2 * m * 16 * 4 + m * 4),
+        ("edge_softmax_h8", lambda: G.edge_softmax(g, s8), (n + 1) * 8 + m * 4 + 2 * m * 8 * 4),
     ]
-    s8 = torch.randn((m, 8), generator=gen, device=dev)
-    cases.append(("edge_softmax_h8", lambda: G.edge_softmax(g, s8),
-                  (n + 1) * 8 + m * 4 + 2 * m * 8 * 4))
     for name, fn, nbytes in cases:
-        t = _time(fn, stream, flush)
+        t, res = _time(fn, stream, flush)
         out[name] = {"ms": round(t, 4), "GB/s": round(nbytes / (t * 1e-3) / 1e9, 1)}
+        keep[name] = res
+    up8 = torch.randn((m, 8), generator=gen, device=dev)
+    alpha = keep["edge_softmax_h8"]
+    t, _ = _time(lambda: kernels.edge_softmax_backward(g, alpha, up8), stream, flush)
+    out["edge_softmax_h8_bwd"] = {"ms": round(t, 4),
+                                  "GB/s": round(((n + 1) * 8 + m * 4 + 3 * m * 8 * 4)
+                                                / (t * 1e-3) / 1e9, 1)}
     labels = torch.randint(0, CLASSES, (n,), generator=gen, device=dev)
     gcn = layers.GCNModel([F, HIDDEN, CLASSES], seed=0, device=dev)
     out["gcn_epoch_ms"] = round(_time(lambda: layers.train_epoch(g, X, labels, gcn, 0.01),
-                                      stream, flush, reps=3), 3)
+                                      stream, flush, reps=3)[0], 3)
     gcn_af = layers.GCNModel([F, HIDDEN, CLASSES], seed=0, device=dev, order="aggregate_first")
     out["gcn_epoch_aggregate_first_ms"] = round(
-        _time(lambda: layers.train_epoch(g, X, labels, gcn_af, 0.01), stream, flush, reps=3), 3)
+        _time(lambda: layers.train_epoch(g, X, labels, gcn_af, 0.01), stream, flush, reps=3)[0], 3)
     sage = layers.SAGEModel([F, HIDDEN, CLASSES], seed=0, device=dev)
     out["sage_epoch_ms"] = round(_time(lambda: layers.train_epoch(g, X, labels, sage, 0.01),
-                                       stream, flush, reps=3), 3)
+                                       stream, flush, reps=3)[0], 3)
     gat = layers.GATModel([F, HIDDEN, HIDDEN, CLASSES], heads=1, seed=0, device=dev)
     out["gat_epoch_ms"] = round(_time(lambda: layers.train_epoch(g, X, labels, gat, 0.01),
-                                      stream, flush, reps=3), 3)
-    return out
+                                      stream, flush, reps=3)[0], 3)
+    return out, keep
+
+
+def run_multi(torch, dist, distributed, pg, X, n, F, flush, stream, dev, rank):
+    """N > 1: the row-partitioned GCN epoch (DistGCN) and the shard exchange
+    alone (all-gather of the d-wide shards), max over ranks."""
+    labels = torch.randint(0, CLASSES, (n,), device=dev, generator=torch.Generator(
+        device=dev).manual_seed(2))
+    model = distributed.DistGCN([F, HIDDEN, CLASSES], seed=0, device=dev)
+    xl = X[pg.r0:pg.r1].contiguous()
+    yl = labels[pg.r0:pg.r1]
+
+    def max_ms(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = torch.tensor([float(np.median(ts))], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    epoch = max_ms(lambda: model.train_epoch(pg, xl, yl, 0.01))
+    ag = max_ms(lambda: pg.all_gather(xl))
+    inbound = (pg.world - 1) * pg.width * F * 4
+    return {"gcn_epoch_ms": round(epoch, 3), "all_gather_ms": round(ag, 3),
+            "all_gather_inbound_bytes": int(inbound),
+            "nvlink_frac": round(inbound / (ag * 1e-3) / 1e9 / NVLINK_GBS, 4),
+            "stages": 1 + len(pg.stage_blocks)}
+
+
+def cpu_leg(torch, args, s, d, adj, X, z_head, outs, extras, n, m, F):
+    """The reference on bounded samples: the parity gate and CPU timings."""
+    indptr, indices, eids = (a.astype(np.int64) for a in adj.numpy())
+    ref = RefCPU()
+    dev = X.device
+
+    def rows_of(t, rows):
+        return t.index_select(0, torch.as_tensor(rows, device=dev)).cpu().numpy()
+
+    parity = {"reference": ref.kind}
+    # headline: copy_u + sum, d = 602
+    smp = RowSample(indptr, indices, eids, args.cpu_edges)
+    x_used = rows_of(X, smp.used).astype(np.float64)
+    z, _, dt = ref.gspmm(smp, "copy_lhs", "sum", smp.pad(x_used))
+    parity["headline"] = dict(compare(rows_of(z_head, smp.rows), z), sample=smp.describe())
+    cpu = {"value": round(spmm_bytes(smp.rows.size, smp.m, F) / dt / 1e9, 3), "unit": "GB/s",
+           "cores": ref.cores, "kind": ref.kind, "seconds": round(dt, 2),
+           "sample": smp.describe() + ", d=%d, %s node_parallel, %d workers (the same sample "
+                     "as --impl reference)" % (F, "graphmp" if ref.kind == "reference"
+                                              else "oracle port", ref.cores)}
+    if not outs:
+        parity["ok"] = parity["headline"]["ok"]
+        return cpu, parity
+    small = RowSample(indptr, indices, eids, 20_000_000)
+    x16u = rows_of(outs["x16"], small.used).astype(np.float64)
+    # copy_u + sum / max at d = 16
+    z, _, dt = ref.gspmm(small, "copy_lhs", "sum", small.pad(x16u))
+    zg = outs["copy_u_sum_d16"][0]
+    parity["copy_u_sum_d16"] = dict(compare(rows_of(zg, small.rows), z), sample=small.describe())
+    extras["copy_u_sum_d16"]["cpu"] = {"GB/s": round(spmm_bytes(small.rows.size, small.m, 16)
+                                                     / dt / 1e9, 3), "s": round(dt, 2)}
+    z, arg, dt = ref.gspmm(small, "copy_lhs", "max", small.pad(x16u))
+    zg, aux = outs["copy_u_max_d16"]
+    parity["copy_u_max_d16"] = dict(merge(compare(rows_of(zg, small.rows), z, exact=True),
+                                          compare(rows_of(aux.arg_edge, small.rows), arg,
+                                                  exact=True)),
+                                    sample=small.describe())
+    extras["copy_u_max_d16"]["cpu"] = {"GB/s": round((spmm_bytes(small.rows.size, small.m, 16)
+                                                      + small.rows.size * 128) / dt / 1e9, 3),
+                                       "s": round(dt, 2)}
+    # u_mul_e + sum at d = 602 (scalar edge weight)
+    wsmp = RowSample(indptr, indices, eids, 3_000_000)
+    xw = wsmp.pad(rows_of(X, wsmp.used).astype(np.float64))
+    w = rows_of(outs["w1"], wsmp.geid).astype(np.float64)
+    z, _, dt = ref.gspmm(wsmp, "mul", "sum", xw, W=w)
+    parity["u_mul_e_sum_d%d" % F] = dict(compare(rows_of(outs["u_mul_e_sum_d%d" % F][0],
+                                                         wsmp.rows), z), sample=wsmp.describe())
+    extras["u_mul_e_sum_d%d" % F]["cpu"] = {
+        "GB/s": round((spmm_bytes(wsmp.rows.size, wsmp.m, F) + 8 * wsmp.m) / dt / 1e9, 3),
+        "s": round(dt, 2)}
+    # u_dot_v g-SDDMM at d = 16
+    es = EdgeSample(s, d, 20_000_000)
+    xe = rows_of(outs["x16"], es.nodes).astype(np.float64)
+    mm, dt = ref.gsddmm_dot(es, xe)
+    parity["u_dot_v_d16"] = dict(compare(rows_of(outs["u_dot_v_d16"], es.geid), mm),
+                                 sample=es.describe())
+    extras["u_dot_v_d16"]["cpu"] = {"GB/s": round((2 * es.m * 4 + 2 * es.m * 64 + es.m * 4)
+                                                  / dt / 1e9, 3), "s": round(dt, 2)}
+    # edge_softmax, 8 heads
+    ssm = RowSample(indptr, indices, eids, 6_000_000)
+    sc = rows_of(outs["s8"], ssm.geid).astype(np.float64)
+    a, dt = ref.edge_softmax(ssm, sc)
+    parity["edge_softmax_h8"] = dict(compare(rows_of(outs["edge_softmax_h8"], ssm.geid), a),
+                                     sample=ssm.describe())
+    extras["edge_softmax_h8"]["cpu"] = {"GB/s": round(((ssm.rows.size + 1) * 8 + ssm.m * 4 +
+                                                       2 * ssm.m * 32) / dt / 1e9, 3),
+                                        "s": round(dt, 2)}
+    for k in ("gcn_epoch_ms", "sage_epoch_ms", "gat_epoch_ms"):
+        extras[k + "_cpu"] = ("not timed: one reference epoch on the Reddit-shaped graph runs "
+                              ">= 145 s of kernels (SURVEY A.4: 123.7 s for the d=602 "
+                              "aggregation alone); the per-op CPU numbers above cover its kernels")
+    parity["cores"] = ref.cores
+    parity["ok"] = all(v["ok"] for v in parity.values() if isinstance(v, dict))
+    return cpu, parity
 
 
 if __name__ == "__main__":

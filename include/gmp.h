@@ -335,6 +335,15 @@ const char* gmp_strerror(int status);
 uint64_t gmp_launch_count(void);
 int gmp_version(void);
 
+/* ---- measurement ------------------------------------------------------------
+ * L2 gather probe (no reference counterpart; the roofline denominator of the
+ * row kernel): n_gathers random rows of row_bytes (64 or 256) from data
+ * (rows x row_bytes, 16 B aligned), 8 rows in flight per lane group at full
+ * occupancy. Time it with events on `stream`; GB/s = n_gathers * row_bytes / t.
+ * sink: one float the kernel may write (keeps the loads live). */
+int gmp_probe_l2_gather(const void* data, int64_t rows, int32_t row_bytes, int64_t n_gathers,
+                        float* sink, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,7 @@ EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "g
             "gmp_extrema_bwd_workspace_size", "gmp_extrema_bwd_copy", "gmp_gather_rows", "gmp_neighbor_sample",
             "gmp_edge_softmax_uv_stats", "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
             "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
-            "gmp_version")
+            "gmp_version", "gmp_probe_l2_gather")
 
 
 class GmpAdj(ctypes.Structure):
@@ -108,6 +108,7 @@ def _declare(lib):
                                            _P(GmpOperand), _P(GmpOperand), vp, i64, i32, i64, vp,
                                            ctypes.c_size_t, vp]
     lib.gmp_unpack_tiles.argtypes = [i64, i32, c_int, i32, vp, vp, i64, vp]
+    lib.gmp_probe_l2_gather.argtypes = [vp, i64, i32, i64, vp, vp]
     lib.gmp_last_error.restype = ctypes.c_char_p
     lib.gmp_strerror.argtypes = [c_int]
     lib.gmp_strerror.restype = ctypes.c_char_p
@@ -117,7 +118,7 @@ def _declare(lib):
                  "gmp_edge_softmax_bwd", "gmp_route_extrema", "gmp_extrema_bwd_copy",
                  "gmp_gather_rows", "gmp_neighbor_sample", "gmp_edge_softmax_uv_stats",
                  "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
-                 "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_version"):
+                 "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_version", "gmp_probe_l2_gather"):
         getattr(lib, name).restype = c_int
 
 

@@ -26,6 +26,7 @@ cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const
                                     const int32_t*, int64_t, void*, int64_t, void*, size_t,
                                     cudaStream_t);
 size_t extrema_workspace_bytes(int64_t cells);
+cudaError_t launch_l2_gather_probe(const void*, int64_t, int32_t, int64_t, float*, cudaStream_t);
 size_t schedule_workspace_bytes(int64_t n);
 cudaError_t launch_gather_rows(int, int64_t, int32_t, const int32_t*, const void*, int64_t, void*,
                                int64_t, cudaStream_t);
@@ -899,6 +900,18 @@ int gmp_neighbor_sample(const int64_t* indptr, int64_t n_rows, const int64_t* se
                                          (cudaStream_t)stream);
   g_launches++;
   return cuda_status(e, "gmp_neighbor_sample");
+}
+
+int gmp_probe_l2_gather(const void* data, int64_t rows, int32_t row_bytes, int64_t n_gathers,
+                        float* sink, void* stream) {
+  if (row_bytes != 64 && row_bytes != 256) return fail(GMP_EINVAL, "row_bytes must be 64 or 256");
+  if (rows <= 0 || rows >= (1ll << 32) || n_gathers < 0) return fail(GMP_EINVAL, "bad sizes");
+  if (!data || !sink) return fail(GMP_EINVAL, "null arrays");
+  if (!aligned(data, 16)) return fail(GMP_EINVAL, "data must be 16-byte aligned");
+  cudaError_t e = launch_l2_gather_probe(data, rows, row_bytes, n_gathers, sink,
+                                         (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_probe_l2_gather");
 }
 
 }  // extern "C"

@@ -679,4 +679,48 @@ cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_
   return err;
 }
 
+
+// ---- L2 gather probe -----------------------------------------------------------
+// The ceiling the row kernel's gathers run against once a column tile of X is
+// L2-resident: n random rows of row_bytes (64 or 256) gathered from a slice
+// of `rows` rows, L = row_bytes / 16 lanes x float4 per row, 8 rows in flight
+// per lane group, full occupancy. Indices come from a splitmix64 hash of the
+// gather number (no index array: the row kernel's indices stream from HBM,
+// which this probe does not charge). bench.py times it live beside the
+// kernel it bounds.
+template <int L>
+__global__ void __launch_bounds__(256) l2_gather_probe_kernel(const float4* __restrict__ data,
+                                                              uint32_t rows, int64_t n,
+                                                              float* sink) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & (L - 1);
+  const int64_t groups = (int64_t)gridDim.x * blockDim.x / L;
+  float acc = 0.f;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / L; g * U < n; g += groups) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint64_t x = (uint64_t)(g * U + u + 1) * 0x9E3779B97F4A7C15ull;
+      x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 29;
+      const uint32_t r = (uint32_t)(x % rows);
+      v[u] = __ldg(data + (int64_t)r * L + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) sink[0] = acc;  // keeps the loads live
+}
+
+cudaError_t launch_l2_gather_probe(const void* data, int64_t rows, int32_t row_bytes, int64_t n,
+                                   float* sink, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (row_bytes == 256)
+    l2_gather_probe_kernel<16><<<sms * 8, 256, 0, s>>>((const float4*)data, (uint32_t)rows, n, sink);
+  else
+    l2_gather_probe_kernel<4><<<sms * 8, 256, 0, s>>>((const float4*)data, (uint32_t)rows, n, sink);
+  return cudaGetLastError();
+}
+
 }  // namespace gmp

@@ -444,13 +444,14 @@ def _staged_call(lib, adj, sched, phi, rho, code, lhs, rhs, Z, ldz, d_out, err, 
                                 Z, ldz, d_out, err, _ptr(tune), stream)
 
 
-def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None):
+def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None, events=None):
     """Aggregation over packed column tiles: gmp_pack_tiles, then one
     gmp_gspmm per 256 B tile (each tile's slice of X stays L2-resident while
     every destination row gathers it; a per-edge scalar is laid out in CSC
     order once and streamed by every tile) writing its columns of Z in place
     (16 B vectors stored as two 8 B halves when Z's rows are only 8 B
-    aligned)."""
+    aligned). `events` (measurement): a list that receives one (start, end)
+    pair of CUDA events recorded around each tile launch."""
     lib = _lib.load()
     dev = g.device
     n = g.num_nodes
@@ -476,10 +477,16 @@ def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None):
     for t in range(nt):
         w = min(tile, d_out - t * tile)
         lhs = _lib.GmpOperand(Xp[t].data_ptr(), tile, w, _lib.TARGETS["src"])
+        if events is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(torch.cuda.current_stream(dev))
         _lib.check(_staged_call(lib, adj, sched, phi, rho, code, lhs, rhs,
                                 Z.data_ptr() + t * tile * F, ldz, w,
                                 err.data_ptr() if err is not None else None, None, stream,
                                 stage, col0=t * tile), "gmp_gspmm")
+        if events is not None:
+            ev[1].record(torch.cuda.current_stream(dev))
+            events.append(ev)
     if err is not None:
         pos = int(err.item())
         if pos != _INT32_MAX:

@@ -51,6 +51,10 @@ out = {
     "algorithmic_bytes_per_launch": alg,
     "row_kernel_l2_hit_pct": sum(x["l2_hit_pct"] for x in row) / max(1, len(row)),
     "row_kernel_l2_read_bytes": sum(x["l2_read_sectors"] for x in row) * 32,
+    "row_kernel_dram_bytes_per_launch": sum(x["dram_read"] + x["dram_write"] for x in row)
+    / max(1, len(row)),
+    "row_kernel_l2_read_bytes_per_launch": sum(x["l2_read_sectors"] for x in row) * 32
+    / max(1, len(row)),
     "serialized_ms": sum(x["ms"] for x in step),
     "per_launch": step,
     "note": "per_launch is one bench step (ncu replay, cold cache); dram_bytes_per_launch is the "

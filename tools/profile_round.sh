@@ -1,9 +1,10 @@
 #!/bin/bash
 # Profiles committed under profiles/ (run on the GPU box through gpurun):
+#   usage: tools/profile_round.sh [ROUND_TAG]
 #   launch list of the default bench command, full ncu capture of one
 #   headline step (summaries only: the .ncu-rep stays in /tmp on the box).
 set -u
-OUT=gpurun_out/prof
+OUT=gpurun_out/prof${1:+_$1}
 mkdir -p $OUT
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/bench_under_ncu.log 2>&1
