@@ -684,7 +684,7 @@ cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_
 // The ceiling the row kernel's gathers run against once a column tile of X is
 // L2-resident: n random rows of row_bytes (64 or 256) gathered from a slice
 // of `rows` rows, L = row_bytes / 16 lanes x float4 per row, 8 rows in flight
-// per lane group, full occupancy. Indices come from a splitmix64 hash of the
+// per lane group, full occupancy. Indices come from a 32-bit hash of the
 // gather number (no index array: the row kernel's indices stream from HBM,
 // which this probe does not charge). bench.py times it live beside the
 // kernel it bounds.
@@ -700,9 +700,12 @@ __global__ void __launch_bounds__(256) l2_gather_probe_kernel(const float4* __re
     float4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      uint64_t x = (uint64_t)(g * U + u + 1) * 0x9E3779B97F4A7C15ull;
-      x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 29;
-      const uint32_t r = (uint32_t)(x % rows);
+      // 32-bit murmur finaliser + multiply-high range reduction: a few
+      // integer ops per gather (a 64-bit modulo is ~100 instructions and made
+      // an earlier version of this probe issue-bound far below the ceiling)
+      uint32_t x = (uint32_t)(g * U + u) * 0x9E3779B1u + 0x7F4A7C15u;
+      x ^= x >> 16; x *= 0x85EBCA6Bu; x ^= x >> 13; x *= 0xC2B2AE35u; x ^= x >> 16;
+      const uint32_t r = __umulhi(x, rows);
       v[u] = __ldg(data + (int64_t)r * L + lane);
     }
 #pragma unroll
