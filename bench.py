@@ -680,7 +680,42 @@ def run_extras(G, kernels, g, X, n, m, flush, stream, dev):
     gat = layers.GATModel([F, HIDDEN, HIDDEN, CLASSES], heads=1, seed=0, device=dev)
     out["gat_epoch_ms"] = round(_time(lambda: layers.train_epoch(g, X, labels, gat, 0.01),
                                       stream, flush, reps=3)[0], 3)
+    out.update(run_minibatch(g, X, labels, n, dev))
     return out, keep
+
+
+def run_minibatch(g, X, labels, n, dev):
+    """The paper's mini-batch benchmarks on the same graph:
+    one NS epoch of 2-layer GraphSAGE (fanouts 25 / 10, 1024 seeds per batch,
+    a fixed 66 % training split - Reddit's) and one CS epoch of 2-layer GCN
+    (1500 contiguous-id clusters, 20 per batch: Cluster-GCN's Reddit setting).
+    Wall time of the whole epoch on the device (sampling included)."""
+    import torch
+    from paper_1909_01315_b200 import layers, minibatch
+    F = X.shape[1]
+    perm = torch.randperm(n, generator=torch.Generator().manual_seed(3))
+    train = perm[:int(n * 0.66)].to(dev)
+    res = {}
+    sage = layers.SAGEModel([F, HIDDEN, CLASSES], seed=0, device=dev)
+    minibatch.train_ns_epoch(g, X, labels, sage, 0.01, train[:4096], 1024, [25, 10])  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    loss, nb = minibatch.train_ns_epoch(g, X, labels, sage, 0.01, train, 1024, [25, 10], seed=1)
+    float(loss)
+    res["ns_sage_epoch_s"] = round(time.perf_counter() - t0, 4)
+    res["ns_batches"] = nb
+    gcn = layers.GCNModel([F, HIDDEN, CLASSES], seed=0, device=dev)
+    parts = minibatch.cluster_partition(n, 1500)
+    mask = torch.zeros(n, dtype=torch.bool, device=dev)
+    mask[train] = True
+    minibatch.train_cs_epoch(g, X, labels, gcn, 0.01, parts[:40], 20, mask)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    loss, nb = minibatch.train_cs_epoch(g, X, labels, gcn, 0.01, parts, 20, mask, seed=1)
+    float(loss)
+    res["cs_gcn_epoch_s"] = round(time.perf_counter() - t0, 4)
+    res["cs_batches"] = nb
+    return res
 
 
 def run_multi(torch, dist, distributed, pg, X, n, F, flush, stream, dev, rank):

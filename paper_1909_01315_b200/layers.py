@@ -242,12 +242,15 @@ class GCNModel:
     def parameters(self):
         return [t for lp in self.layers for t in (lp.W, lp.b)]
 
+    def layer(self, i, g, h, **kw):
+        """Layer i on graph g (a full graph or a sampled block)."""
+        return gcn_layer(g, h, self.layers[i], act="relu" if i < len(self.layers) - 1 else "linear",
+                         aggregator=self.aggregator, order=self.order, **kw)
+
     def forward(self, g, x, **kw):
         h = x
-        last = len(self.layers) - 1
-        for i, p in enumerate(self.layers):
-            h = gcn_layer(g, h, p, act="relu" if i < last else "linear",
-                          aggregator=self.aggregator, order=self.order, **kw)
+        for i in range(len(self.layers)):
+            h = self.layer(i, g, h, **kw)
         return h
 
 
@@ -268,12 +271,15 @@ class SAGEModel:
     def parameters(self):
         return [t for lp in self.layers for t in (lp.W_self, lp.W_neigh)]
 
+    def layer(self, i, g, h, **kw):
+        return sage_layer(g, h, self.layers[i],
+                          act="relu" if i < len(self.layers) - 1 else "linear", order=self.order,
+                          **kw)
+
     def forward(self, g, x, **kw):
         h = x
-        last = len(self.layers) - 1
-        for i, p in enumerate(self.layers):
-            h = sage_layer(g, h, p, act="relu" if i < last else "linear", order=self.order,
-                           **kw)
+        for i in range(len(self.layers)):
+            h = self.layer(i, g, h, **kw)
         return h
 
 
@@ -305,13 +311,14 @@ class GATModel:
     def parameters(self):
         return [t for p in self.layers for hp in p.heads for t in (hp.W, hp.a_l, hp.a_r)]
 
+    def layer(self, i, g, h, **kw):
+        h = gat_layer(g, h, self.layers[i], fused=self.fused, **kw)
+        return torch.relu(h) if i < len(self.layers) - 1 else h
+
     def forward(self, g, x, **kw):
         h = x
-        last = len(self.layers) - 1
-        for i, p in enumerate(self.layers):
-            h = gat_layer(g, h, p, fused=self.fused, **kw)
-            if i < last:
-                h = torch.relu(h)
+        for i in range(len(self.layers)):
+            h = self.layer(i, g, h, **kw)
         return h
 
 
