@@ -160,6 +160,27 @@ int gmp_gspmm_staged(const gmp_adj* adj, const gmp_sched* sched, int op, int rho
                      void* Z, int64_t ldz, int32_t d_out, int32_t* err_pos,
                      const gmp_tuning* tuning, void* stream);
 
+/* ---- heavy rows over the bulk-copy ring (one packed column tile) ----------
+ * The packed-tile aggregation of kernels._gspmm_tiled (the wide copy_u /
+ * u_mul_e path; replaces the same _GroupedWalk segment reduction,
+ * kernels.py:340-466, for one 256 B column slice): heavy rows (schedule
+ * prefix, degree > heavy_threshold) stream their 256 B source rows through a
+ * shared-memory ring fed by cp.async.bulk, one persistent CTA per SM, chunk
+ * partials merged in fixed order; the other rows run the row kernel.
+ * Conditions: dtype GMP_F32; op GMP_COPY_LHS (lhs GMP_SRC) or GMP_MUL (lhs
+ * GMP_SRC, rhs a GMP_EDGE_POS scalar); rho GMP_SUM / GMP_MEAN; lhs rows are
+ * 64 floats (ld == 64, 16 B aligned); d_out <= 64. Results equal gmp_gspmm's
+ * (fp64 accumulation of the exact messages, one rounding).
+ * The workspace is sized by gmp_gspmm_ring_workspace_size and filled once
+ * per (adjacency, schedule) by gmp_gspmm_ring_prepare; it is then reused by
+ * every call on that adjacency (calls on one stream; not concurrently). */
+size_t gmp_gspmm_ring_workspace_size(const gmp_adj* adj, const gmp_sched* sched);
+int gmp_gspmm_ring_prepare(const gmp_adj* adj, const gmp_sched* sched, void* ws,
+                           size_t ws_bytes, void* stream);
+int gmp_gspmm_ring(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
+                   const gmp_operand* lhs, const gmp_operand* rhs, void* Z, int64_t ldz,
+                   int32_t d_out, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- g-SDDMM ------------------------------------------------------------
  * Replaces kernels.gsddmm (kernels.py:744-836), default strategy
  * edge_parallel over COO (_gsddmm_chunked, kernels.py:732-741):

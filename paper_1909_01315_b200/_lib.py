@@ -26,7 +26,8 @@ EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "g
             "gmp_extrema_bwd_workspace_size", "gmp_extrema_bwd_copy", "gmp_gather_rows", "gmp_neighbor_sample",
             "gmp_edge_softmax_uv_stats", "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
             "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
-            "gmp_version", "gmp_probe_l2_gather")
+            "gmp_version", "gmp_probe_l2_gather", "gmp_gspmm_ring_workspace_size",
+            "gmp_gspmm_ring_prepare", "gmp_gspmm_ring")
 
 
 class GmpAdj(ctypes.Structure):
@@ -109,6 +110,12 @@ def _declare(lib):
                                            ctypes.c_size_t, vp]
     lib.gmp_unpack_tiles.argtypes = [i64, i32, c_int, i32, vp, vp, i64, vp]
     lib.gmp_probe_l2_gather.argtypes = [vp, i64, i32, i64, vp, vp]
+    lib.gmp_gspmm_ring_workspace_size.argtypes = [_P(GmpAdj), _P(GmpSched)]
+    lib.gmp_gspmm_ring_workspace_size.restype = ctypes.c_size_t
+    lib.gmp_gspmm_ring_prepare.argtypes = [_P(GmpAdj), _P(GmpSched), vp, ctypes.c_size_t, vp]
+    lib.gmp_gspmm_ring.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, c_int, c_int,
+                                   _P(GmpOperand), _P(GmpOperand), vp, i64, i32, vp,
+                                   ctypes.c_size_t, vp]
     lib.gmp_last_error.restype = ctypes.c_char_p
     lib.gmp_strerror.argtypes = [c_int]
     lib.gmp_strerror.restype = ctypes.c_char_p
@@ -118,7 +125,8 @@ def _declare(lib):
                  "gmp_edge_softmax_bwd", "gmp_route_extrema", "gmp_extrema_bwd_copy",
                  "gmp_gather_rows", "gmp_neighbor_sample", "gmp_edge_softmax_uv_stats",
                  "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
-                 "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_version", "gmp_probe_l2_gather"):
+                 "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_version", "gmp_probe_l2_gather",
+                 "gmp_gspmm_ring_prepare", "gmp_gspmm_ring"):
         getattr(lib, name).restype = c_int
 
 

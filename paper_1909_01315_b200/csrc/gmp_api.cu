@@ -16,6 +16,7 @@
 #include "softmax.cuh"
 #include "spmm_dot.cuh"
 #include "spmm_rows.cuh"
+#include "spmm_ring.cuh"
 
 namespace gmp {
 template <int OP>
@@ -51,6 +52,7 @@ cudaError_t launch_pack_tiles(int, bool, int64_t, int32_t, int32_t, const void*,
 cudaError_t launch_neighbor_sample(const int64_t*, const int64_t*, int64_t, const int64_t*, uint64_t,
                                    int64_t*, int64_t*, cudaStream_t);
 int softmax_window_resident_ctas(int f64, int V, bool bwd);
+
 cudaError_t build_schedule(int64_t n, const int64_t* indptr, int32_t thr, int32_t light,
                            int32_t* order_out, void* ws, size_t ws_bytes, int64_t* n_heavy,
                            int64_t* n_medium, int64_t* n_nonempty, int64_t* max_degree,
@@ -497,6 +499,64 @@ int gmp_gspmm_staged(const gmp_adj* adj, const gmp_sched* sched, int op, int rho
   Staged st{acc, ldacc, flags, deg_full};
   return gspmm_impl(adj, sched, op, rho, dtype, lhs, rhs, Z, ldz, d_out, nullptr, nullptr,
                     err_pos, tuning, stream, &st);
+}
+
+size_t gmp_gspmm_ring_workspace_size(const gmp_adj* adj, const gmp_sched* sched) {
+  if (!adj || !sched || sched->n_heavy <= 0) return 0;
+  return ring_workspace_bytes(sched->n_heavy, adj->m);
+}
+
+int gmp_gspmm_ring_prepare(const gmp_adj* adj, const gmp_sched* sched, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (!adj || !sched) return fail(GMP_EINVAL, "null adjacency / schedule");
+  if (sched->n_heavy <= 0) return GMP_OK;
+  if (!sched->order) return fail(GMP_EINVAL, "schedule has heavy rows but no order");
+  if (!ws || ws_bytes < gmp_gspmm_ring_workspace_size(adj, sched))
+    return fail(GMP_EINVAL, "ring workspace too small");
+  cudaError_t e = launch_ring_prepare(adj->indptr, sched->order, sched->n_heavy, ws,
+                                      (cudaStream_t)stream);
+  g_launches++;
+  return cuda_status(e, "gmp_gspmm_ring_prepare");
+}
+
+int gmp_gspmm_ring(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
+                   const gmp_operand* lhs, const gmp_operand* rhs, void* Z, int64_t ldz,
+                   int32_t d_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!adj || !sched || !lhs) return fail(GMP_EINVAL, "null adjacency / schedule / operand");
+  if (dtype != GMP_F32) return fail(GMP_EUNSUPPORTED, "the ring path is fp32");
+  if (rho != GMP_SUM && rho != GMP_MEAN) return fail(GMP_EUNSUPPORTED, "the ring path is sum / mean");
+  const bool mul = op == GMP_MUL;
+  if (op != GMP_COPY_LHS && !mul) return fail(GMP_EUNSUPPORTED, "the ring path is copy_u / u_mul_e");
+  if (lhs->target != GMP_SRC || lhs->ld != 64 || !aligned(lhs->data, 16))
+    return fail(GMP_EINVAL, "ring lhs must be packed 64-float source rows, 16 B aligned");
+  if (mul && (!rhs || rhs->target != GMP_EDGE_POS || rhs->dim != 1))
+    return fail(GMP_EINVAL, "ring u_mul_e takes a per-position scalar rhs");
+  if (d_out < 1 || d_out > 64 || ldz < d_out || !Z) return fail(GMP_EINVAL, "bad d_out / Z");
+  const int64_t nh = sched->n_heavy;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nh > 0) {
+    if (!ws || ws_bytes < gmp_gspmm_ring_workspace_size(adj, sched))
+      return fail(GMP_EINVAL, "ring workspace too small");
+    RingArgs a{};
+    a.indptr = adj->indptr; a.indices = adj->indices; a.order = sched->order; a.n_heavy = nh;
+    a.X = static_cast<const float*>(lhs->data);
+    a.W = mul ? static_cast<const float*>(rhs->data) : nullptr;
+    a.Z = static_cast<float*>(Z); a.ldz = ldz; a.width = d_out; a.mean = rho == GMP_MEAN;
+    cudaError_t e = launch_ring(mul, a, ws, s);
+    g_launches += 2;
+    if (e != cudaSuccess) return cuda_status(e, "gmp_gspmm_ring");
+  }
+  if (nh >= adj->n_rows) return GMP_OK;
+  // the remaining rows: the row kernel over the schedule without its heavy prefix
+  gmp_sched lt = *sched;
+  lt.order = sched->order ? sched->order + nh : nullptr;
+  lt.n_heavy = 0;
+  lt.n_medium = std::max<int64_t>(0, sched->n_medium - nh);
+  lt.n_nonempty = std::max<int64_t>(0, sched->n_nonempty - nh);
+  gmp_adj la = *adj;
+  la.n_rows = adj->n_rows - nh;
+  return gspmm_impl(&la, &lt, op, rho, dtype, lhs, rhs, Z, ldz, d_out, nullptr, nullptr, nullptr,
+                    nullptr, stream, nullptr);
 }
 
 int gmp_gsddmm(const gmp_coo* coo, int op, int dtype, const gmp_operand* lhs, const gmp_operand* rhs,

@@ -23,6 +23,7 @@ Differences that are the point of the port:
 """
 
 import ctypes
+import os
 import threading
 from contextlib import contextmanager
 from dataclasses import dataclass
@@ -444,6 +445,30 @@ def _staged_call(lib, adj, sched, phi, rho, code, lhs, rhs, Z, ldz, d_out, err, 
                                 Z, ldz, d_out, err, _ptr(tune), stream)
 
 
+_RING_OFF = bool(os.environ.get("GMP_NO_RING"))
+
+
+def _ring_workspace(adj, sched, stream):
+    """Workspace of the heavy-row bulk-copy ring (gmp_gspmm_ring), prepared
+    once per adjacency and cached with it; None when the schedule has no
+    heavy rows (or GMP_NO_RING is set)."""
+    if _RING_OFF or sched.n_heavy <= 0:
+        return None
+    # one workspace per stream: calls on a stream are ordered; concurrent
+    # callers on other streams get their own counter and partials
+    key = ("ring_ws", stream.value)
+    ws = adj._extra.get(key)
+    if ws is None:
+        lib = _lib.load()
+        a, sc = ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct)
+        nbytes = int(lib.gmp_gspmm_ring_workspace_size(a, sc))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=adj.indptr.device)
+        _lib.check(lib.gmp_gspmm_ring_prepare(a, sc, ws.data_ptr(), nbytes, stream),
+                   "gmp_gspmm_ring_prepare")
+        adj._extra[key] = ws
+    return ws
+
+
 def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None, events=None):
     """Aggregation over packed column tiles: gmp_pack_tiles, then one
     gmp_gspmm per 256 B tile (each tile's slice of X stays L2-resident while
@@ -474,16 +499,24 @@ def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None, events=None):
     _lib.check(lib.gmp_pack_tiles(n_src, d_out, code, tile, X.data_ptr(), _ld(X), Xp.data_ptr(),
                                   stream), "gmp_pack_tiles")
     ldz = _ld(Z)
+    ring = _ring_workspace(adj, sched, stream) if (
+        stage is None and F == 4 and phi.op in ("copy_lhs", "mul")) else None
     for t in range(nt):
         w = min(tile, d_out - t * tile)
         lhs = _lib.GmpOperand(Xp[t].data_ptr(), tile, w, _lib.TARGETS["src"])
         if events is not None:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record(torch.cuda.current_stream(dev))
-        _lib.check(_staged_call(lib, adj, sched, phi, rho, code, lhs, rhs,
-                                Z.data_ptr() + t * tile * F, ldz, w,
-                                err.data_ptr() if err is not None else None, None, stream,
-                                stage, col0=t * tile), "gmp_gspmm")
+        if ring is not None:
+            _lib.check(lib.gmp_gspmm_ring(ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct),
+                                          _lib.OPS[phi.op], _lib.RHOS[rho], code, ctypes.byref(lhs),
+                                          _ptr(rhs), Z.data_ptr() + t * tile * F, ldz, w,
+                                          ring.data_ptr(), ring.numel(), stream), "gmp_gspmm_ring")
+        else:
+            _lib.check(_staged_call(lib, adj, sched, phi, rho, code, lhs, rhs,
+                                    Z.data_ptr() + t * tile * F, ldz, w,
+                                    err.data_ptr() if err is not None else None, None, stream,
+                                    stage, col0=t * tile), "gmp_gspmm")
         if events is not None:
             ev[1].record(torch.cuda.current_stream(dev))
             events.append(ev)
@@ -508,6 +541,24 @@ def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None, stage=None):
             torch.empty((n, d_out), dtype=ref.dtype, device=dev))
         _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage)
         return Z, (g.to_csc().degrees().clone() if rho == "mean" else None)
+    if (stage is None and tune is None and phi.op == "copy_lhs" and phi.lhs_target == "src"
+            and rho in ("sum", "mean") and X.dtype == torch.float32 and 32 < d_out <= 64
+            and n > 0 and _ld(X) == 64 and X.data_ptr() % 16 == 0):
+        # already-packed 256 B source rows (a host-pipeline tile, or d = 64):
+        # heavy rows over the bulk-copy ring
+        adj = g.to_csc()
+        sched = adj.schedule()
+        ring = _ring_workspace(adj, sched, _stream(dev))
+        if ring is not None:
+            Z = out if out is not None else accounting.register(
+                torch.empty((n, d_out), dtype=ref.dtype, device=dev))
+            lhs = _lib.GmpOperand(X.data_ptr(), 64, d_out, _lib.TARGETS["src"])
+            _lib.check(lib.gmp_gspmm_ring(ctypes.byref(_adj_struct(adj)),
+                                          ctypes.byref(sched.struct), _lib.OPS["copy_lhs"],
+                                          _lib.RHOS[rho], _lib.GMP_F32, ctypes.byref(lhs), None,
+                                          Z.data_ptr(), _ld(Z), d_out, ring.data_ptr(),
+                                          ring.numel(), _stream(dev)), "gmp_gspmm_ring")
+            return Z, (adj.degrees().clone() if rho == "mean" else None)
     Z = out if out is not None else accounting.register(
         torch.empty((n, d_out), dtype=ref.dtype, device=dev))
     arg = None

@@ -41,7 +41,12 @@ def test_tiled_copy_matches_oracle(small_budget, dtype, d, ld, rho):
     tile = 256 // base.itemsize
     aligned = ld % tile == 0
     if not aligned:
-        assert launches == 1 + -(-d // tile), launches  # pack + one launch per tile
+        nt = -(-d // tile)
+        if dtype == np.float32 and g.to_csc().schedule().n_heavy > 0 and not kernels._RING_OFF:
+            # pack + ring prepare (first call) + per tile: ring, merge, row kernel
+            assert launches == 2 + 3 * nt, launches
+        else:
+            assert launches == 1 + nt, launches  # pack + one launch per tile
     want, wcnt = O.gspmm(s, dd, n, "copy_lhs", "src", None, rho, X=base[:, :d].astype(np.float64))
     if dtype == np.float32:
         assert np.allclose(to_np(Z), want, rtol=RTOL32, atol=ATOL32)
