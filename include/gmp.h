@@ -160,13 +160,15 @@ int gmp_gspmm_staged(const gmp_adj* adj, const gmp_sched* sched, int op, int rho
                      void* Z, int64_t ldz, int32_t d_out, int32_t* err_pos,
                      const gmp_tuning* tuning, void* stream);
 
-/* ---- heavy rows over the bulk-copy ring (one packed column tile) ----------
+/* ---- heavy rows over the TMA gather4 ring (one packed column tile) --------
  * The packed-tile aggregation of kernels._gspmm_tiled (the wide copy_u /
  * u_mul_e path; replaces the same _GroupedWalk segment reduction,
  * kernels.py:340-466, for one 256 B column slice): heavy rows (schedule
- * prefix, degree > heavy_threshold) stream their 256 B source rows through a
- * shared-memory ring fed by cp.async.bulk, one persistent CTA per SM, chunk
- * partials merged in fixed order; the other rows run the row kernel.
+ * prefix, degree > heavy_threshold) stream their 256 B source rows through
+ * per-warp shared-memory rings fed by cp.async.bulk.tensor tile::gather4,
+ * one persistent CTA per SM, chunk partials merged in fixed order; the other
+ * rows run the row kernel. n_src_rows = rows of the packed lhs (its tensor
+ * map's extent).
  * Conditions: dtype GMP_F32; op GMP_COPY_LHS (lhs GMP_SRC) or GMP_MUL (lhs
  * GMP_SRC, rhs a GMP_EDGE_POS scalar); rho GMP_SUM / GMP_MEAN; lhs rows are
  * 64 floats (ld == 64, 16 B aligned); d_out <= 64. Results equal gmp_gspmm's
@@ -178,8 +180,8 @@ size_t gmp_gspmm_ring_workspace_size(const gmp_adj* adj, const gmp_sched* sched)
 int gmp_gspmm_ring_prepare(const gmp_adj* adj, const gmp_sched* sched, void* ws,
                            size_t ws_bytes, void* stream);
 int gmp_gspmm_ring(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
-                   const gmp_operand* lhs, const gmp_operand* rhs, void* Z, int64_t ldz,
-                   int32_t d_out, void* ws, size_t ws_bytes, void* stream);
+                   const gmp_operand* lhs, const gmp_operand* rhs, int64_t n_src_rows, void* Z,
+                   int64_t ldz, int32_t d_out, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- g-SDDMM ------------------------------------------------------------
  * Replaces kernels.gsddmm (kernels.py:744-836), default strategy

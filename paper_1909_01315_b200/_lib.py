@@ -114,7 +114,7 @@ def _declare(lib):
     lib.gmp_gspmm_ring_workspace_size.restype = ctypes.c_size_t
     lib.gmp_gspmm_ring_prepare.argtypes = [_P(GmpAdj), _P(GmpSched), vp, ctypes.c_size_t, vp]
     lib.gmp_gspmm_ring.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, c_int, c_int,
-                                   _P(GmpOperand), _P(GmpOperand), vp, i64, i32, vp,
+                                   _P(GmpOperand), _P(GmpOperand), i64, vp, i64, i32, vp,
                                    ctypes.c_size_t, vp]
     lib.gmp_last_error.restype = ctypes.c_char_p
     lib.gmp_strerror.argtypes = [c_int]

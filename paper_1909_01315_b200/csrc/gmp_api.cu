@@ -520,9 +520,10 @@ int gmp_gspmm_ring_prepare(const gmp_adj* adj, const gmp_sched* sched, void* ws,
 }
 
 int gmp_gspmm_ring(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, int dtype,
-                   const gmp_operand* lhs, const gmp_operand* rhs, void* Z, int64_t ldz,
-                   int32_t d_out, void* ws, size_t ws_bytes, void* stream) {
+                   const gmp_operand* lhs, const gmp_operand* rhs, int64_t n_src_rows, void* Z,
+                   int64_t ldz, int32_t d_out, void* ws, size_t ws_bytes, void* stream) {
   if (!adj || !sched || !lhs) return fail(GMP_EINVAL, "null adjacency / schedule / operand");
+  if (n_src_rows < 1 || n_src_rows >= (1ll << 31)) return fail(GMP_EINVAL, "bad n_src_rows");
   if (dtype != GMP_F32) return fail(GMP_EUNSUPPORTED, "the ring path is fp32");
   if (rho != GMP_SUM && rho != GMP_MEAN) return fail(GMP_EUNSUPPORTED, "the ring path is sum / mean");
   const bool mul = op == GMP_MUL;
@@ -542,7 +543,7 @@ int gmp_gspmm_ring(const gmp_adj* adj, const gmp_sched* sched, int op, int rho, 
     a.X = static_cast<const float*>(lhs->data);
     a.W = mul ? static_cast<const float*>(rhs->data) : nullptr;
     a.Z = static_cast<float*>(Z); a.ldz = ldz; a.width = d_out; a.mean = rho == GMP_MEAN;
-    cudaError_t e = launch_ring(mul, a, ws, s);
+    cudaError_t e = launch_ring(mul, a, n_src_rows, ws, s);
     g_launches += 2;
     if (e != cudaSuccess) return cuda_status(e, "gmp_gspmm_ring");
   }

@@ -445,13 +445,17 @@ def _staged_call(lib, adj, sched, phi, rho, code, lhs, rhs, Z, ldz, d_out, err, 
                                 Z, ldz, d_out, err, _ptr(tune), stream)
 
 
-_RING_OFF = bool(os.environ.get("GMP_NO_RING"))
+# The heavy-row TMA gather4 ring (spmm_ring.cu) is opt-in (GMP_RING=1): it is
+# correct and deterministic, but measured slower than the register-gather row
+# kernel on the Reddit-shaped headline (copy_u d=602: 28.1 vs 23.8 ms; u_mul_e
+# 41.0 vs 36.1 ms at 16 warps / SM; profiles/r02_tma_ring.json, DESIGN 3.1).
+_RING_OFF = os.environ.get("GMP_RING", "0") in ("", "0")
 
 
 def _ring_workspace(adj, sched, stream):
-    """Workspace of the heavy-row bulk-copy ring (gmp_gspmm_ring), prepared
+    """Workspace of the heavy-row TMA gather4 ring (gmp_gspmm_ring), prepared
     once per adjacency and cached with it; None when the schedule has no
-    heavy rows (or GMP_NO_RING is set)."""
+    heavy rows or the ring is not enabled (GMP_RING=1)."""
     if _RING_OFF or sched.n_heavy <= 0:
         return None
     # one workspace per stream: calls on a stream are ordered; concurrent
@@ -510,7 +514,7 @@ def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None, events=None):
         if ring is not None:
             _lib.check(lib.gmp_gspmm_ring(ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct),
                                           _lib.OPS[phi.op], _lib.RHOS[rho], code, ctypes.byref(lhs),
-                                          _ptr(rhs), Z.data_ptr() + t * tile * F, ldz, w,
+                                          _ptr(rhs), n_src, Z.data_ptr() + t * tile * F, ldz, w,
                                           ring.data_ptr(), ring.numel(), stream), "gmp_gspmm_ring")
         else:
             _lib.check(_staged_call(lib, adj, sched, phi, rho, code, lhs, rhs,
@@ -545,7 +549,7 @@ def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None, stage=None):
             and rho in ("sum", "mean") and X.dtype == torch.float32 and 32 < d_out <= 64
             and n > 0 and _ld(X) == 64 and X.data_ptr() % 16 == 0):
         # already-packed 256 B source rows (a host-pipeline tile, or d = 64):
-        # heavy rows over the bulk-copy ring
+        # heavy rows over the TMA gather4 ring
         adj = g.to_csc()
         sched = adj.schedule()
         ring = _ring_workspace(adj, sched, _stream(dev))
@@ -556,7 +560,7 @@ def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None, stage=None):
             _lib.check(lib.gmp_gspmm_ring(ctypes.byref(_adj_struct(adj)),
                                           ctypes.byref(sched.struct), _lib.OPS["copy_lhs"],
                                           _lib.RHOS[rho], _lib.GMP_F32, ctypes.byref(lhs), None,
-                                          Z.data_ptr(), _ld(Z), d_out, ring.data_ptr(),
+                                          X.shape[0], Z.data_ptr(), _ld(Z), d_out, ring.data_ptr(),
                                           ring.numel(), _stream(dev)), "gmp_gspmm_ring")
             return Z, (adj.degrees().clone() if rho == "mean" else None)
     Z = out if out is not None else accounting.register(
