@@ -139,6 +139,8 @@ int hub_cluster(const gmp_adj* adj, const gmp_sched* sched, int width) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
+  static const int forced = getenv("GMP_CLUSTER") ? atoi(getenv("GMP_CLUSTER")) : 0;
+  if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
   return sched->max_degree * 2 * (int64_t)sms > adj->m ? 8 : 1;
 }
 

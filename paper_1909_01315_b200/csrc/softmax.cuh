@@ -100,9 +100,12 @@ template <> struct ColSum<double> {
 // one warp step.
 constexpr int kChunk = 256;
 
+#ifndef GMP_STATS_U4
+#define GMP_STATS_U4 4
+#endif
 template <int V>
 struct StatsUnroll {
-  static constexpr int value = V == 4 ? 4 : 8;
+  static constexpr int value = V == 4 ? GMP_STATS_U4 : 8;
 };
 
 // Pass 1 of the statistics for edges [pb, pe) of one row owned by this warp

@@ -35,6 +35,7 @@
 // messages compare the fp64 message, so arg edges equal the reference's.
 #pragma once
 
+#include <cstdlib>
 #include <type_traits>
 
 #include <cooperative_groups.h>
@@ -44,6 +45,12 @@
 namespace gmp {
 
 constexpr int kWarpsPerCta = 8;
+#ifndef GMP_PIPE_MIN_BLOCKS
+#define GMP_PIPE_MIN_BLOCKS 3
+#endif
+#ifndef GMP_PIPE_NB
+#define GMP_PIPE_NB 4
+#endif
 #ifndef GMP_ROW_MIN_BLOCKS
 #define GMP_ROW_MIN_BLOCKS 3
 #endif
@@ -244,13 +251,23 @@ struct Policy {
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-// s + c += x exactly (TwoSum, Knuth); packed fp32x2.
+// a - b on packed fp32x2: FADD2 with a negated operand (two register
+// sources; an FFMA2 by -1 has three and issues at half the rate)
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
+// s + c += x exactly (TwoSum, Knuth); packed fp32x2, seven FADD2.
 __device__ __forceinline__ void two_sum2(float2& s, float2& c, float2 x) {
-  const float2 m1 = f2(-1.f, -1.f);
   const float2 t = __fadd2_rn(s, x);
-  const float2 bb = __ffma2_rn(s, m1, t);                      // t - s
-  const float2 e1 = __ffma2_rn(__ffma2_rn(bb, m1, t), m1, s);  // s - (t - bb)
-  const float2 e2 = __ffma2_rn(bb, m1, x);                     // x - bb
+  const float2 bb = fsub2(t, s);               // t - s
+  const float2 e1 = fsub2(s, fsub2(t, bb));    // s - (t - bb)
+  const float2 e2 = fsub2(x, bb);              // x - bb
   c = __fadd2_rn(c, __fadd2_rn(e1, e2));
   s = t;
 }
@@ -335,11 +352,9 @@ struct RowAcc {
             float2 y = f2((float)b[k], (float)b[k + 1]);
             if constexpr (OP == OP_SUB) y = f2(-y.x, -y.y);
             // exact message x + y = t + r, then accumulate both parts
-            const float2 m1 = f2(-1.f, -1.f);
             const float2 t = __fadd2_rn(x, y);
-            const float2 bb = __ffma2_rn(x, m1, t);
-            const float2 r = __fadd2_rn(__ffma2_rn(__ffma2_rn(bb, m1, t), m1, x),
-                                        __ffma2_rn(bb, m1, y));
+            const float2 bb = fsub2(t, x);
+            const float2 r = __fadd2_rn(fsub2(x, fsub2(t, bb)), fsub2(y, bb));
             two_sum2(S, C, t);
             C = __fadd2_rn(C, r);
           }
@@ -554,6 +569,109 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
     }
     nb0 = nb1; eb0 = eb1; nb1 = nb2; eb1 = eb2;
     sa0 = sa1; sb0 = sb1;
+  }
+  acc.fold();
+}
+
+// Software-pipelined accumulate for the packed-tile shape: 16 feature lanes
+// per edge slot (E = 2), one float4 per lane, i.e. one 256 B tile row per
+// edge - the Reddit-shaped headline and every wide copy_u / u_mul_e sum.
+// spmm_accumulate issues a burst of U gathers, waits for all of them and
+// then runs the compensated sums, so a warp has nothing in flight while it
+// computes. Here every lane keeps a ring of NB float4 registers: step k
+// consumes ring slot k % NB and immediately refills it with the gather of
+// step k + NB (taken from the next 32-edge batch's neighbour ids near the end
+// of a batch), so NB - 1..NB gathers stay in flight through the arithmetic.
+// Same edge order per slot and the same fold points (every 2 batches = 32
+// edges per slot) as spmm_accumulate: the results are bit-identical.
+// Operands: lhs gathered by neighbour id; rhs none (copy) or a per-edge scalar
+// addressed by position or neighbour id (no edge ids needed).
+template <int OP, int MP, int NB>
+__device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t pb, int64_t pe,
+                                                     int64_t first, int64_t stride, int lane,
+                                                     int slot, int col, bool valid,
+                                                     const float (&rc)[3],
+                                                     RowAcc<float, OP, RHO_SUM, 4>& acc) {
+  static_assert(16 % NB == 0, "ring slots must be compile-time across a batch");
+  constexpr bool SC = OP != OP_COPY;  // per-edge scalar rhs
+  const int64_t base = pb + first;
+  if (base >= pe) return;
+  const int64_t nbatch = (pe - base + stride - 1) / stride;
+  const int32_t* __restrict__ indices = a.indices;
+  const float* lcol = static_cast<const float*>(a.lhs.data) + (valid ? col : 0);
+  const uint32_t lld = a.lhs.ld * (uint32_t)sizeof(float);
+  const bool r_pos = a.rhs.from_pos;
+  // lane L of a batch register holds edge 2 (L & 15) + (L >> 4) of the batch:
+  // slot s reads edge 2k + s with a width-16 shuffle from lane k (an
+  // immediate lane, no per-step lane arithmetic); the loads stay coalesced
+  const int pl = 2 * (lane & 15) + (lane >> 4);
+  auto ld_idx = [&](int64_t bb) -> int32_t {
+    return bb + pl < pe ? __ldg(indices + bb + pl) : 0;
+  };
+  auto ld_sc = [&](int64_t bb, int32_t nb) -> float {
+    if constexpr (SC) {
+      if (bb + pl < pe) {
+        double ts = 0.0;
+        return rhs_scalar<float, MP>(a, r_pos ? (uint32_t)(bb + pl) : (uint32_t)nb, rc, ts);
+      }
+    }
+    return 0.f;
+  };
+  auto gather = [&](int32_t nbreg, int k) -> float4 {
+    const uint32_t r = (uint32_t)__shfl_sync(kFull, nbreg, k, 16);
+    return __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(lcol) +
+                                                 (uint64_t)r * lld));
+  };
+  int32_t cur = ld_idx(base);
+  int32_t nxt = nbatch > 1 ? ld_idx(base + stride) : 0;
+  float wcur = ld_sc(base, cur);
+  float4 buf[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) buf[k] = gather(cur, k);
+
+  for (int64_t b = 0; b < nbatch; ++b) {
+    const int64_t bb = base + b * stride;
+    const bool more = b + 1 < nbatch;
+    const int32_t nn = b + 2 < nbatch ? ld_idx(bb + 2 * stride) : 0;
+    const float wnxt = more ? ld_sc(bb + stride, nxt) : 0.f;
+    const int64_t rem64 = pe - bb;
+    const int rem = rem64 < 32 ? (int)rem64 : 32;
+    auto steps = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int j = 2 * k + slot;
+        const bool use = FULL || j < rem;
+        const float4 x = buf[k % NB];
+        float va[4] = {x.x, x.y, x.z, x.w};
+        float vb[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (SC) {
+          const float w = __shfl_sync(kFull, wcur, k, 16);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) vb[q] = w;
+        }
+        if constexpr (!FULL) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            va[q] = use ? va[q] : 0.f;
+            vb[q] = use ? vb[q] : 0.f;
+          }
+        }
+        // refill this ring slot with step k + NB
+        if (k + NB < 16) {
+          buf[k % NB] = gather(cur, k + NB);
+        } else if (more) {
+          buf[k % NB] = gather(nxt, k + NB - 16);
+        }
+        acc.add(va, vb, true, 0);
+      }
+    };
+    if (rem == 32) steps(std::true_type{});
+    else steps(std::false_type{});
+    if (b & 1) acc.fold();
+    cur = nxt;
+    nxt = nn;
+    wcur = wnxt;
   }
   acc.fold();
 }
@@ -834,8 +952,8 @@ struct Unroll {
 // share a warp and longer rows stage edge ids in shared memory. Wide kernels
 // (every d >= 16 with V=4, and all fp64 launches) compile without those paths
 // so their main loop is scheduled on its own.
-template <typename T, int OP, int RHO, int V, int MP, bool NARROW>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, GMP_ROW_MIN_BLOCKS)
+template <typename T, int OP, int RHO, int V, int MP, bool NARROW, bool PIPE = false>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, PIPE ? GMP_PIPE_MIN_BLOCKS : GMP_ROW_MIN_BLOCKS)
 spmm_rows_kernel(const SpmmArgs a) {
   using Acc = RowAcc<T, OP, RHO, V>;
   using ExtT = typename Acc::ExtT;
@@ -952,12 +1070,21 @@ spmm_rows_kernel(const SpmmArgs a) {
   } else if (row_const) {
     // nothing to accumulate
   } else if (heavy) {
-    spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, ((int64_t)crank * kWarpsPerCta + warp) * 32,
-                                          (int64_t)32 * kWarpsPerCta * ncl, lane, slot, E, col,
-                                          valid, ha, hb, rc, acc);
+    if constexpr (PIPE)
+      spmm_accumulate_pipe<OP, MP, GMP_PIPE_NB>(a, pb, pe,
+                                                ((int64_t)crank * kWarpsPerCta + warp) * 32,
+                                                (int64_t)32 * kWarpsPerCta * ncl, lane, slot, col,
+                                                valid, rc, acc);
+    else
+      spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, ((int64_t)crank * kWarpsPerCta + warp) * 32,
+                                            (int64_t)32 * kWarpsPerCta * ncl, lane, slot, E, col,
+                                            valid, ha, hb, rc, acc);
   } else {
-    spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, 0, 32, lane, slot, E, col, valid, ha, hb,
-                                          rc, acc);
+    if constexpr (PIPE)
+      spmm_accumulate_pipe<OP, MP, GMP_PIPE_NB>(a, pb, pe, 0, 32, lane, slot, col, valid, rc, acc);
+    else
+      spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, 0, 32, lane, slot, E, col, valid, ha, hb,
+                                            rc, acc);
   }
   acc.combine_slots(a.g_log2);
   if constexpr (MP == MP_AB) {  // every lane summed alpha*w of its own edges
@@ -1098,6 +1225,13 @@ cudaError_t launch_rows_cfg(Kern kern, const SpmmArgs& a, int64_t grid, size_t s
 
 template <typename T, int OP, int RHO, int V, int MP>
 cudaError_t launch_spmm_rows_t(const SpmmArgs& a, int64_t grid, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4 && V == 4 && RHO == RHO_SUM &&
+                ((OP == OP_COPY && MP == MP_F) || (OP == OP_MUL && MP == MP_FS))) {
+    // one 256 B tile row per edge (16 lanes x float4): the pipelined gather ring
+    static const bool off = getenv("GMP_NO_PIPE") != nullptr;
+    if (!off && a.g_log2 == 4 && !a.need_eid)
+      return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false, true>, a, grid, 0, s);
+  }
   if constexpr (sizeof(T) == 4) {
     if (narrow_launch<V>(a.g_log2))
       return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, true>, a, grid,
