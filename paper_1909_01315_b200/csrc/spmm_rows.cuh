@@ -594,10 +594,11 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
                                                      RowAcc<float, OP, RHO_SUM, 4>& acc) {
   static_assert(16 % NB == 0, "ring slots must be compile-time across a batch");
   constexpr bool SC = OP != OP_COPY;  // per-edge scalar rhs
-  const int64_t base = pb + first;
-  if (base >= pe) return;
-  const int64_t nbatch = (pe - base + stride - 1) / stride;
-  const int32_t* __restrict__ indices = a.indices;
+  // 32-bit offsets relative to the batch start (a row has < 2^31 edges)
+  if (pb + first >= pe) return;
+  const int32_t* __restrict__ ip = a.indices + pb + first;
+  int32_t left = (int32_t)(pe - pb - first);  // edges from the current batch start on
+  const int32_t step = (int32_t)stride;
   const float* lcol = static_cast<const float*>(a.lhs.data) + (valid ? col : 0);
   const uint32_t lld = a.lhs.ld * (uint32_t)sizeof(float);
   const bool r_pos = a.rhs.from_pos;
@@ -605,14 +606,14 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
   // slot s reads edge 2k + s with a width-16 shuffle from lane k (an
   // immediate lane, no per-step lane arithmetic); the loads stay coalesced
   const int pl = 2 * (lane & 15) + (lane >> 4);
-  auto ld_idx = [&](int64_t bb) -> int32_t {
-    return bb + pl < pe ? __ldg(indices + bb + pl) : 0;
-  };
-  auto ld_sc = [&](int64_t bb, int32_t nb) -> float {
+  // index of batch edge pl at batch offset o (0 past the row: row 0, harmless)
+  auto ld_idx = [&](int32_t o) -> int32_t { return pl + o < left ? __ldg(ip + o + pl) : 0; };
+  auto ld_sc = [&](int32_t o, int32_t nb) -> float {
     if constexpr (SC) {
-      if (bb + pl < pe) {
+      if (pl + o < left) {
         double ts = 0.0;
-        return rhs_scalar<float, MP>(a, r_pos ? (uint32_t)(bb + pl) : (uint32_t)nb, rc, ts);
+        const int64_t q = (ip - a.indices) + o + pl;  // CSC position
+        return rhs_scalar<float, MP>(a, r_pos ? (uint32_t)q : (uint32_t)nb, rc, ts);
       }
     }
     return 0.f;
@@ -622,26 +623,21 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
     return __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(lcol) +
                                                  (uint64_t)r * lld));
   };
-  int32_t cur = ld_idx(base);
-  int32_t nxt = nbatch > 1 ? ld_idx(base + stride) : 0;
-  float wcur = ld_sc(base, cur);
+  int32_t cur = ld_idx(0);
+  int32_t nxt = ld_idx(step);
+  float wcur = ld_sc(0, cur);
   float4 buf[NB];
 #pragma unroll
   for (int k = 0; k < NB; ++k) buf[k] = gather(cur, k);
 
-  for (int64_t b = 0; b < nbatch; ++b) {
-    const int64_t bb = base + b * stride;
-    const bool more = b + 1 < nbatch;
-    const int32_t nn = b + 2 < nbatch ? ld_idx(bb + 2 * stride) : 0;
-    const float wnxt = more ? ld_sc(bb + stride, nxt) : 0.f;
-    const int64_t rem64 = pe - bb;
-    const int rem = rem64 < 32 ? (int)rem64 : 32;
+  for (int b = 0;; ++b) {
+    const int32_t nn = ld_idx(2 * step);
+    const float wnxt = ld_sc(step, nxt);
     auto steps = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        const int j = 2 * k + slot;
-        const bool use = FULL || j < rem;
+        const bool use = FULL || 2 * k + slot < left;
         const float4 x = buf[k % NB];
         float va[4] = {x.x, x.y, x.z, x.w};
         float vb[4] = {0.f, 0.f, 0.f, 0.f};
@@ -657,18 +653,18 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
             vb[q] = use ? vb[q] : 0.f;
           }
         }
-        // refill this ring slot with step k + NB
-        if (k + NB < 16) {
-          buf[k % NB] = gather(cur, k + NB);
-        } else if (more) {
-          buf[k % NB] = gather(nxt, k + NB - 16);
-        }
+        // refill this ring slot with step k + NB (the next batch's ids near
+        // the end; past the last batch they are 0: row 0, never used)
+        buf[k % NB] = k + NB < 16 ? gather(cur, k + NB) : gather(nxt, k + NB - 16);
         acc.add(va, vb, true, 0);
       }
     };
-    if (rem == 32) steps(std::true_type{});
+    if (left >= 32) steps(std::true_type{});
     else steps(std::false_type{});
     if (b & 1) acc.fold();
+    left -= step;
+    if (left <= 0) break;
+    ip += step;
     cur = nxt;
     nxt = nn;
     wcur = wnxt;
