@@ -426,22 +426,14 @@ static int gspmm_impl(const gmp_adj* adj, const gmp_sched* sched, int op, int rh
   // 32 lanes; otherwise every non-heavy row gets a warp
   const int E = 32 / G;
   const bool narrow = (F == 4) && narrow_launch_host(V, log2i(G));
-  const int64_t n_medium = (order && narrow) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
-  const int64_t medium_blocks = (n_medium - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
-  const int64_t light_rows = adj->n_rows - n_medium;
   // a copy of the destination's own row reads no edges (row-constant path)
   const bool row_const = kop == OP_COPY && ops[0].dev.target == GMP_DST;
   const int ncl = hub_cluster(adj, sched, row_const ? 0 : tw);
-  const int64_t bpt_rows = round_up(
-      n_heavy * ncl + medium_blocks +
-          (light_rows + (int64_t)kWarpsPerCta * E - 1) / ((int64_t)kWarpsPerCta * E),
-      ncl);
   SpmmArgs a{};
   a.cluster = ncl;
   a.z_split = z_split;
   a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
-  a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_medium;
-  a.medium_blocks = medium_blocks; a.blocks_per_tile = bpt_rows;
+  a.n_rows = adj->n_rows; a.n_heavy = n_heavy;
   a.d_out = d_out; a.tile_cols = tw; a.g_log2 = log2i(G); a.mean = rho == GMP_MEAN;
   a.lhs = row_operand(ops[0]);
   a.rhs = row_operand(ops[1]);
@@ -459,6 +451,21 @@ static int gspmm_impl(const gmp_adj* adj, const gmp_sched* sched, int op, int rh
   }
   a.need_eid = ext || (a.lhs.from_eid && a.lhs.mode != M_HOIST) ||
                (ops[1].present && a.rhs.from_eid && a.rhs.mode != M_HOIST);
+  // light rows (degree <= the schedule's light threshold) share a warp, one
+  // per lane group, in the narrow kernels and in the pipelined 256 B-row
+  // kernel (launch_spmm_rows_t picks it by the same predicate)
+  const bool pipe = F == 4 && pipe_launch(V, krho, kop, mp, a.g_log2, a.need_eid);
+  const int64_t n_medium =
+      (order && (narrow || pipe)) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
+  const int64_t medium_blocks = (n_medium - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int64_t light_rows = adj->n_rows - n_medium;
+  const int64_t bpt_rows = round_up(
+      n_heavy * ncl + medium_blocks +
+          (light_rows + (int64_t)kWarpsPerCta * E - 1) / ((int64_t)kWarpsPerCta * E),
+      ncl);
+  a.n_medium = n_medium;
+  a.medium_blocks = medium_blocks;
+  a.blocks_per_tile = bpt_rows;
   a.Z = Z; a.ldz = ldz; a.arg = arg; a.counts = counts; a.err_pos = err_pos;
   if (stg) {
     a.acc64 = stg->acc; a.ldacc = stg->ldacc; a.acc_mode = stg->mode; a.deg_full = stg->deg_full;

@@ -981,7 +981,9 @@ spmm_rows_kernel(const SpmmArgs a) {
   const int64_t heavy_blocks = a.n_heavy * ncl;
   const bool heavy = local < heavy_blocks;  // block-uniform
   const int crank = heavy ? (int)(local % ncl) : 0;
-  const bool light = NARROW && local >= heavy_blocks + a.medium_blocks;  // block-uniform
+  // light rows share a warp, one per lane group (NARROW kernels; the PIPE
+  // kernel's two 16-lane slots take one light row each)
+  const bool light = (NARROW || PIPE) && local >= heavy_blocks + a.medium_blocks;  // block-uniform
 
   int64_t row;
   if (heavy) {
@@ -1037,6 +1039,15 @@ spmm_rows_kernel(const SpmmArgs a) {
 #pragma unroll
         for (int k = 0; k < V; ++k) acc.acc[k] = (double)deg * (double)ha[k];
       }
+    }
+  }
+  if constexpr (PIPE) {
+    if (light) {
+      spmm_accumulate_slot<T, OP, RHO, V, MP, GMP_PIPE_NB>(a, pb, pe, col, valid, ha, hb, rc, acc);
+      if (row < 0) return;
+      if (a.counts && tile == 0 && gl == 0) a.counts[row] = deg;
+      write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
+      return;
     }
   }
   if (row_const) {
@@ -1219,13 +1230,21 @@ cudaError_t launch_rows_cfg(Kern kern, const SpmmArgs& a, int64_t grid, size_t s
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+// fp32 launches that take the pipelined gather ring (spmm_accumulate_pipe):
+// sum / mean of copy_u or u_mul_e (per-edge scalar) with one 256 B tile row
+// per edge (16 lanes x float4) and no edge ids. The host sizes the grid by
+// the same predicate (light rows two per warp). GMP_NO_PIPE=1 disables it.
+inline bool pipe_launch(int V, int rho, int op, int mp, int g_log2, int need_eid) {
+  static const bool off = getenv("GMP_NO_PIPE") != nullptr;
+  return !off && V == 4 && rho == RHO_SUM && g_log2 == 4 && !need_eid &&
+         ((op == OP_COPY && mp == MP_F) || (op == OP_MUL && mp == MP_FS));
+}
+
 template <typename T, int OP, int RHO, int V, int MP>
 cudaError_t launch_spmm_rows_t(const SpmmArgs& a, int64_t grid, cudaStream_t s) {
   if constexpr (sizeof(T) == 4 && V == 4 && RHO == RHO_SUM &&
                 ((OP == OP_COPY && MP == MP_F) || (OP == OP_MUL && MP == MP_FS))) {
-    // one 256 B tile row per edge (16 lanes x float4): the pipelined gather ring
-    static const bool off = getenv("GMP_NO_PIPE") != nullptr;
-    if (!off && a.g_log2 == 4 && !a.need_eid)
+    if (pipe_launch(V, RHO, OP, MP, a.g_log2, a.need_eid))
       return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false, true>, a, grid, 0, s);
   }
   if constexpr (sizeof(T) == 4) {
