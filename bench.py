@@ -605,7 +605,7 @@ def kernel_roofline(torch, kernels, _lib, g, X, n, m, F, value, ms, peak, peak_k
         "achieved": round(achieved, 1), "peak": round(ceiling, 1), "frac": round(achieved / ceiling, 4),
         "peak_kind": "measured live: gmp_probe_l2_gather, %d random 256 B rows from a %.1f MB "
                      "slice (best of 3)" % (m, n * 256 / 2 ** 20),
-        "kernel": "spmm_rows_kernel<float,COPY,SUM,V=4,MP_F> over one packed 256 B column tile",
+        "kernel": "spmm_rows_kernel<float,COPY,SUM,V=4,MP_F,PIPE> (register gather ring) over one packed 256 B column tile",
         "bytes_per_launch": gathered,
         "bytes_model": "m x 256 B: one 256 B packed tile row gathered per edge (whole sectors)",
         "launch_ms": round(t_tile, 4), "launches_per_step": ntiles,
