@@ -327,6 +327,23 @@ int gmp_extrema_bwd_binary(const gmp_coo* coo, int64_t n_rows, int32_t d, int dt
 int gmp_gather_rows(int64_t n, int32_t dim, int dtype, const int32_t* idx, const void* src,
                     int64_t lds, void* dst, int64_t ldd, void* stream);
 
+/* dst[p, :] = src[eids[p], :] for every position p of the adjacency (the
+ * same result as gmp_gather_rows with idx = adj->eids), reading src one
+ * L2-sized window of consecutive edge ids at a time: heavy rows are walked
+ * per (window, row) - their positions inside a window are one contiguous run
+ * when every row's edge ids ascend - so each src line is fetched from DRAM
+ * about once; rows after the heavy prefix (through n_nonempty) gather
+ * directly. Requires sched->sorted_eids == adj->eids when sched->n_heavy > 0
+ * (callers use gmp_gather_rows otherwise). workspace: per-(heavy row, window)
+ * bounds, gmp_gather_adj_workspace_size bytes. Replaces the per-call
+ * fancy-index gather of an edge operand into chunk order
+ * (kernels.py:255-296, _gather of W by edge id). */
+size_t gmp_gather_adj_workspace_size(const gmp_adj* adj, const gmp_sched* sched, int32_t dim,
+                                     int dtype);
+int gmp_gather_adj(const gmp_adj* adj, const gmp_sched* sched, int32_t dim, int dtype,
+                   const void* src, int64_t lds, void* dst, int64_t ldd, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
 /* ---- column-tile packing ----------------------------------------------------
  * tile: a power of two >= 2.
  * packed (ceil(d/tile), n, tile): packed[t][r][c] = src[r][t*tile + c], zero

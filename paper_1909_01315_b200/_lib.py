@@ -27,7 +27,8 @@ EXPORTED = ("gmp_schedule_workspace_size", "gmp_build_schedule", "gmp_gspmm", "g
             "gmp_edge_softmax_uv_stats", "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
             "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_last_error", "gmp_strerror", "gmp_launch_count",
             "gmp_version", "gmp_probe_l2_gather", "gmp_gspmm_ring_workspace_size",
-            "gmp_gspmm_ring_prepare", "gmp_gspmm_ring")
+            "gmp_gspmm_ring_prepare", "gmp_gspmm_ring", "gmp_gather_adj_workspace_size",
+            "gmp_gather_adj")
 
 
 class GmpAdj(ctypes.Structure):
@@ -98,6 +99,10 @@ def _declare(lib):
     lib.gmp_extrema_bwd_copy.argtypes = [i64, i32, c_int, vp, vp, i64, vp, i64, vp, i64, vp,
                                          ctypes.c_size_t, vp]
     lib.gmp_gather_rows.argtypes = [i64, i32, c_int, vp, vp, i64, vp, i64, vp]
+    lib.gmp_gather_adj_workspace_size.argtypes = [_P(GmpAdj), _P(GmpSched), i32, c_int]
+    lib.gmp_gather_adj_workspace_size.restype = ctypes.c_size_t
+    lib.gmp_gather_adj.argtypes = [_P(GmpAdj), _P(GmpSched), i32, c_int, vp, i64, vp, i64, vp,
+                                   ctypes.c_size_t, vp]
     lib.gmp_neighbor_sample.argtypes = [vp, i64, vp, i64, vp, ctypes.c_uint64, vp, vp, vp]
     lib.gmp_edge_softmax_uv_stats.argtypes = [_P(GmpAdj), _P(GmpSched), c_int, vp, i64, vp, i64,
                                               i32, vp, ctypes.c_size_t, vp]
@@ -126,7 +131,7 @@ def _declare(lib):
                  "gmp_gather_rows", "gmp_neighbor_sample", "gmp_edge_softmax_uv_stats",
                  "gmp_gat_aggregate", "gmp_pack_tiles", "gmp_unpack_tiles",
                  "gmp_extrema_bwd_binary", "gmp_rowdot", "gmp_version", "gmp_probe_l2_gather",
-                 "gmp_gspmm_ring_prepare", "gmp_gspmm_ring"):
+                 "gmp_gspmm_ring_prepare", "gmp_gspmm_ring", "gmp_gather_adj"):
         getattr(lib, name).restype = c_int
 
 

@@ -29,6 +29,12 @@ cudaError_t launch_extrema_bwd_copy(int, int64_t, int32_t, const int64_t*, const
 size_t extrema_workspace_bytes(int64_t cells);
 cudaError_t launch_l2_gather_probe(const void*, int64_t, int32_t, int64_t, float*, cudaStream_t);
 size_t schedule_workspace_bytes(int64_t n);
+size_t gather_adj_workspace(int64_t n_heavy, int64_t m, int32_t dim, size_t F, int64_t* nw_out,
+                            int64_t* win_out);
+cudaError_t launch_gather_adj(int f64, const int64_t* indptr, const int32_t* eids,
+                              const int32_t* order, int64_t n_heavy, int64_t n_nonempty, int64_t m,
+                              int32_t dim, const void* src, int64_t lds, void* dst, int64_t ldd,
+                              void* ws, cudaStream_t s);
 cudaError_t launch_gather_rows(int, int64_t, int32_t, const int32_t*, const void*, int64_t, void*,
                                int64_t, cudaStream_t);
 struct ExtBinArgs {
@@ -764,6 +770,33 @@ int gmp_edge_softmax_bwd(const gmp_adj* in_adj, const gmp_coo* coo, const gmp_sc
                          size_t workspace_bytes, void* stream) {
   return softmax_common(in_adj, coo, sched, dtype, alpha, lda, grad, ldg, H, ds, ldds, workspace,
                         workspace_bytes, true, stream);
+}
+
+size_t gmp_gather_adj_workspace_size(const gmp_adj* adj, const gmp_sched* sched, int32_t dim,
+                                     int dtype) {
+  if (!adj || !sched || dim <= 0) return 0;
+  return gather_adj_workspace(sched->n_heavy, adj->m, dim, dtype == GMP_F64 ? 8 : 4, nullptr,
+                              nullptr);
+}
+
+int gmp_gather_adj(const gmp_adj* adj, const gmp_sched* sched, int32_t dim, int dtype,
+                   const void* src, int64_t lds, void* dst, int64_t ldd, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  if (!adj || !sched) return fail(GMP_EINVAL, "null adjacency / schedule");
+  if (dtype != GMP_F32 && dtype != GMP_F64) return fail(GMP_EINVAL, "unknown dtype %d", dtype);
+  if (dim < 1 || lds < dim || ldd < dim) return fail(GMP_EINVAL, "bad sizes");
+  if (adj->m == 0) return GMP_OK;
+  if (!src || !dst || !adj->indptr || !adj->eids) return fail(GMP_EINVAL, "null arrays");
+  if (sched->n_heavy > 0 && (!sched->order || sched->sorted_eids != adj->eids))
+    return fail(GMP_EINVAL, "windowed gather needs the schedule order and row-ascending edge ids "
+                            "(sched->sorted_eids == adj->eids)");
+  if (workspace_bytes < gmp_gather_adj_workspace_size(adj, sched, dim, dtype))
+    return fail(GMP_EINVAL, "workspace too small");
+  cudaError_t e = launch_gather_adj(dtype == GMP_F64, adj->indptr, adj->eids, sched->order,
+                                    sched->n_heavy, sched->n_nonempty, adj->m, dim, src, lds, dst,
+                                    ldd, workspace, (cudaStream_t)stream);
+  g_launches += sched->n_heavy > 0 ? 2 : 1;
+  return cuda_status(e, "gmp_gather_adj");
 }
 
 int gmp_gather_rows(int64_t n, int32_t dim, int dtype, const int32_t* idx, const void* src,

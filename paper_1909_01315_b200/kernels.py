@@ -494,7 +494,7 @@ def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None, events=None):
     rhs = None
     err = None
     if phi.op != "copy_lhs":
-        Wc = _gather_rows(adj.edge_ids, W.to(X.dtype))
+        Wc = _gather_adj(adj, W.to(X.dtype))
         rhs = _lib.GmpOperand(_data_ptr(Wc), 1, 1, _lib.TARGETS["edge_pos"])
         if phi.op == "div":
             err = _err_slot(dev)
@@ -574,7 +574,7 @@ def _gspmm_launch(g, phi, rho, X, Y, W, d_out, tune=None, out=None, stage=None):
     if W is not None and phi.op != "dot" and _permute_edge_scalar(W, d_out):
         # a per-edge scalar re-read by >= 3 column tiles: lay it out in CSC
         # order once so every tile streams it (gmp_gather_rows)
-        Wc = _gather_rows(adj.edge_ids, W)
+        Wc = _gather_adj(adj, W)
         op_w = _lib.GmpOperand(_data_ptr(Wc), 1, 1, _lib.TARGETS["edge_pos"])
         if phi.lhs_target == "edge":
             lhs = op_w
@@ -619,6 +619,37 @@ def _permute_edge_scalar(W, d_out):
     if W.dtype == torch.float64:
         v = min(v, 2)
     return -(-d_out // (32 * v)) >= 3
+
+
+# below this many edges the edge operand fits L2 and the plain gather is as good
+_GATHER_ADJ_MIN_EDGES = 1 << 22
+
+
+def _gather_adj(adj, M):
+    """M's rows in adjacency order, out[p] = M[adj.edge_ids[p]]: the windowed
+    gmp_gather_adj when the adjacency has heavy rows whose edge ids ascend
+    (each window of edge ids is read from DRAM once), else gmp_gather_rows."""
+    sched = adj.schedule() if adj.num_groups > 0 else None
+    if (sched is None or sched.n_heavy == 0 or M.shape[0] < _GATHER_ADJ_MIN_EDGES
+            or _sorted_eids(adj) is not adj.edge_ids):
+        return _gather_rows(adj.edge_ids, M)
+    lib = _lib.load()
+    out = torch.empty((adj.edge_ids.numel(), M.shape[1]), dtype=M.dtype, device=M.device)
+    sc = sched.struct
+    saved = sc.sorted_eids
+    sc.sorted_eids = adj.edge_ids.data_ptr()
+    try:
+        a = ctypes.byref(_adj_struct(adj))
+        nbytes = int(lib.gmp_gather_adj_workspace_size(a, ctypes.byref(sc), M.shape[1],
+                                                       _dtype_code(M)))
+        ws = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=M.device)
+        _lib.check(lib.gmp_gather_adj(a, ctypes.byref(sc), M.shape[1], _dtype_code(M),
+                                      M.data_ptr(), _ld(M), out.data_ptr(), M.shape[1],
+                                      ws.data_ptr(), nbytes, _stream(M.device)),
+                   "gmp_gather_adj")
+    finally:
+        sc.sorted_eids = saved
+    return out
 
 
 def _gather_rows(idx, M):

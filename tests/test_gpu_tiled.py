@@ -110,3 +110,37 @@ def test_tiled_div_by_zero_names_smallest_edge(small_budget):
     with pytest.raises(ZeroDivisionError, match="edge id %d$" % first):
         G.gspmm(g, kernels.MessageFunc("div", "src", "edge"), "sum",
                 X=torch.ones((n, 150), device=DEV), W=w)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("dim", [1, 3])
+def test_windowed_adjacency_gather_equals_plain(monkeypatch, dtype, dim):
+    """gmp_gather_adj (per-(window, heavy row) runs, light rows direct) is
+    the plain gather out[p] = W[eids[p]], bit for bit, on a graph whose rows'
+    edge ids ascend (edges grouped by source) and whose heavy rows span many
+    windows."""
+    monkeypatch.setattr(kernels, "_GATHER_ADJ_MIN_EDGES", 0)
+    s, dd = G.generators.power_law_edges(20000, 60, seed=9)
+    g = G.from_arrays(s, dd, num_nodes=20000, device=DEV)
+    adj = g.to_csc()
+    assert kernels._sorted_eids(adj) is adj.edge_ids and adj.schedule().n_heavy > 0
+    w = torch.as_tensor(np.random.default_rng(1).standard_normal((s.size, dim)).astype(dtype),
+                        device=DEV)
+    got = kernels._gather_adj(adj, w)
+    want = w.index_select(0, adj.edge_ids.to(torch.int64))
+    assert torch.equal(got, want)
+
+
+def test_u_mul_e_with_windowed_gather_matches_oracle(monkeypatch, small_budget):
+    monkeypatch.setattr(kernels, "_GATHER_ADJ_MIN_EDGES", 0)
+    s, dd = G.generators.power_law_edges(20000, 60, seed=9)
+    n = 20000
+    g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((n, 130)).astype(np.float32)
+    w = rng.standard_normal((s.size, 1)).astype(np.float32)
+    Z, _ = G.gspmm(g, kernels.mul("src", "edge"), "sum", X=torch.as_tensor(x, device=DEV),
+                   W=torch.as_tensor(w, device=DEV))
+    want, _ = O.gspmm(s, dd, n, "mul", "src", "edge", "sum", X=x.astype(np.float64),
+                      W=w.astype(np.float64))
+    assert np.allclose(to_np(Z), want, rtol=RTOL32, atol=ATOL32)
