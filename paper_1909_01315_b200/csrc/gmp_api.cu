@@ -728,13 +728,24 @@ static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sche
     w.bounds = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + wp.off_bounds);
     e = launch_edge_softmax_window(F == 8, V, bwd, a, w, st);
     g_launches += 3;
+    // rows [n_heavy, n_medium): one warp each; [n_medium, n_nonempty): one
+    // per lane group (short rows); empty rows have no edge to normalise
+    const int64_t n_med = std::max(n_heavy, std::min(sched->n_medium, sched->n_nonempty));
     SoftmaxArgs lt = a;
     lt.order = a.order + n_heavy;
-    lt.n_rows = adj->n_rows - n_heavy;
+    lt.n_rows = n_med - n_heavy;
     lt.n_heavy = 0;
     lt.blocks_per_tile = (lt.n_rows + kWarpsPerCta - 1) / kWarpsPerCta;
     if (e == cudaSuccess && lt.n_rows > 0) {
       e = launch_edge_softmax(F == 8, V, bwd, uv, lt, lt.blocks_per_tile, st);
+      g_launches++;
+    }
+    SoftmaxArgs sl = a;
+    sl.order = a.order + n_med;
+    sl.n_rows = sched->n_nonempty - n_med;
+    sl.n_heavy = 0;
+    if (e == cudaSuccess && sl.n_rows > 0) {
+      e = launch_edge_softmax_slots(F == 8, V, bwd, uv, sl, st);
       g_launches++;
     }
   } else {

@@ -120,6 +120,33 @@ cudaError_t launch_edge_softmax(int f64, int V, bool bwd, bool uv, const Softmax
   return cudaGetLastError();
 }
 
+template <typename T, bool BWD, bool UV>
+static void softmax_slot_v(int V, const SoftmaxArgs& a, int64_t grid, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {
+    if (V == 4) { edge_softmax_slot_kernel<T, 4, BWD, UV><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a); return; }
+  }
+  if (V == 2) { edge_softmax_slot_kernel<T, 2, BWD, UV><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a); return; }
+  edge_softmax_slot_kernel<T, 1, BWD, UV><<<(unsigned)grid, kWarpsPerCta * 32, 0, s>>>(a);
+}
+
+// short rows, one per lane group: a.n_rows rows of a.order, one column tile
+cudaError_t launch_edge_softmax_slots(int f64, int V, bool bwd, bool uv, const SoftmaxArgs& a,
+                                      cudaStream_t s) {
+  const int64_t per_cta = (int64_t)kWarpsPerCta * (32 >> a.g_log2);
+  const int64_t grid = (a.n_rows + per_cta - 1) / per_cta;
+  if (grid == 0) return cudaSuccess;
+  if (f64) {
+    if (bwd) softmax_slot_v<double, true, false>(V, a, grid, s);
+    else if (uv) softmax_slot_v<double, false, true>(V, a, grid, s);
+    else softmax_slot_v<double, false, false>(V, a, grid, s);
+  } else {
+    if (bwd) softmax_slot_v<float, true, false>(V, a, grid, s);
+    else if (uv) softmax_slot_v<float, false, true>(V, a, grid, s);
+    else softmax_slot_v<float, false, false>(V, a, grid, s);
+  }
+  return cudaGetLastError();
+}
+
 template <typename T, bool BWD>
 static void softmax_window_v(int V, const SoftmaxArgs& a, const WindowArgs& w, unsigned grid,
                              cudaStream_t s) {

@@ -302,6 +302,94 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_kernel(const S
   if (slot == 0 && valid) stats_write<T, V, BWD>(a, row, col, m, l);
 }
 
+// Statistics of short rows (degree <= the schedule's light threshold; on
+// Reddit 106k of the 135k non-empty rows have 1-16 in-edges): one row per
+// lane group (E rows per warp), the row's edges walked U at a time with the
+// same online update as stats_pass1 - no shared-memory staging, no warp
+// combine.
+template <typename T, int V, bool BWD, bool UV>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) edge_softmax_slot_kernel(const SoftmaxArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = 32 >> a.g_log2;
+  const int slot = lane >> a.g_log2, gl = lane & ((1 << a.g_log2) - 1);
+  const int64_t r = ((int64_t)blockIdx.x * kWarpsPerCta + warp) * E + slot;
+  if (r >= a.n_rows) return;  // lanes are independent below
+  const int64_t row = a.order ? (int64_t)a.order[r] : r;
+  const int64_t pb = a.indptr[row], pe = a.indptr[row + 1];
+  if (pe == pb) return;
+  const int col = gl * V;
+  const bool valid = col < a.H;
+  const int ccol = valid ? col : 0;
+  T er_row[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) er_row[k] = T(0);
+  if (UV) load_vec<T, V>(static_cast<const T*>(a.er) + row * a.ldr + ccol, er_row);
+  const T* S = static_cast<const T*>(a.s) + ccol;
+  const T* Gd = static_cast<const T*>(a.g) + ccol;
+  const T* EL = UV ? static_cast<const T*>(a.el) + ccol : nullptr;
+  const int32_t* ids = UV ? a.indices : a.eids;
+  T m[V];
+  ColSum<T> acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) m[k] = -INFINITY;
+  constexpr int U = 4;
+  for (int64_t p0 = pb; p0 < pe; p0 += U) {
+    T x[U][V], gg[U][V];
+    T xl[UV ? U : 1][V];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ok[u] = p0 + u < pe && valid;
+      const int64_t e = ok[u] ? (int64_t)__ldg(ids + p0 + u) : 0;
+#pragma unroll
+      for (int k = 0; k < V; ++k) x[u][k] = gg[u][k] = T(0);
+      if constexpr (UV) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) xl[u][k] = T(0);
+        if (ok[u]) {
+          load_vec<T, V>(EL + e * a.lde, x[u]);
+#pragma unroll
+          for (int k = 0; k < V; ++k) uv_score(x[u][k], er_row[k], x[u][k], xl[u][k]);
+        }
+      } else if (ok[u]) {
+        load_vec<T, V>(S + e * a.lds, x[u]);
+        if constexpr (BWD) load_vec<T, V>(Gd + e * a.ldg, gg[u]);
+      }
+    }
+    if constexpr (BWD) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k].add_prod(x[u][k], gg[u][k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        T mx = m[k];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u] && x[u][k] > mx) mx = x[u][k];
+        if (mx > m[k]) {
+          if (m[k] != T(-INFINITY)) acc[k].scale(sm_exp(m[k], mx));
+          m[k] = mx;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!ok[u]) continue;
+          if constexpr (UV) acc[k].add(sm_exp(x[u][k], xl[u][k], m[k]));
+          else acc[k].add(sm_exp(x[u][k], m[k]));
+        }
+      }
+    }
+  }
+  if (!valid) return;
+  double l[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) l[k] = acc[k].value();
+  stats_write<T, V, BWD>(a, row, col, m, l);
+}
+
 // Windowed statistics for the heavy rows (edge-keyed scores only). A random
 // 32 B score row costs a whole 128 B DRAM line (tools/micro/randread.cu), so
 // walking heavy rows in CSC order moves ~4x the score bytes. Instead the edge
@@ -524,6 +612,8 @@ __global__ void __launch_bounds__(256) edge_softmax_apply_kernel(const SoftmaxAr
 
 cudaError_t launch_edge_softmax(int dtype_is_f64, int V, bool bwd, bool uv, const SoftmaxArgs& a,
                                 int64_t grid, cudaStream_t s);
+cudaError_t launch_edge_softmax_slots(int dtype_is_f64, int V, bool bwd, bool uv,
+                                      const SoftmaxArgs& a, cudaStream_t s);
 cudaError_t launch_edge_softmax_window(int dtype_is_f64, int V, bool bwd, const SoftmaxArgs& a,
                                        const WindowArgs& w, cudaStream_t s);
 cudaError_t launch_edge_softmax_apply(int dtype_is_f64, int V, bool bwd, bool uv,
