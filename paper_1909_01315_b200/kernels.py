@@ -399,6 +399,17 @@ _TILE_BYTES = 256
 _L2_BUDGET = 64 << 20
 
 
+def _tile_cols(n_src, F):
+    """Packed column-tile width: 256 B rows (the pipelined row kernel's
+    shape) unless even that slice of the n_src gathered rows overflows the
+    L2 budget; then 128 B or 64 B rows (e.g. d = 32 / 64 over a million
+    sources: a 256 B-row slice alone is 256 MB), down to 64 B."""
+    t = _TILE_BYTES // F
+    while t * F > 64 and n_src * t * F > _L2_BUDGET:
+        t //= 2
+    return t
+
+
 def _tiled_applies(phi, rho, X, W, d_out, n, tune):
     """Wide src-gathered aggregations whose column slices must be L2-tiled
     (the row kernel's rule) and whose rows are not already aligned 256 B runs:
@@ -418,11 +429,13 @@ def _tiled_applies(phi, rho, X, W, d_out, n, tune):
     if X.shape[1] != d_out:
         return False
     F = X.element_size()
-    tile = _TILE_BYTES // F
     # the gathered slice is X's (source) rows - a row block of a partitioned
     # graph gathers more (or fewer) rows than it has destinations
+    tile = _tile_cols(X.shape[0], F)
     if d_out <= tile or X.shape[0] * d_out * F <= _L2_BUDGET:
         return False
+    if tile < _TILE_BYTES // F:
+        return True  # narrower than one warp pass: the row kernel cannot split it in place
     aligned = _ld(X) % tile == 0 and X.data_ptr() % 16 == 0
     return not aligned
 
@@ -485,7 +498,7 @@ def _gspmm_tiled(g, phi, rho, X, W, Z, d_out, stage=None, events=None):
     dev = g.device
     n = g.num_nodes
     F = X.element_size()
-    tile = _TILE_BYTES // F
+    tile = _tile_cols(X.shape[0], F)
     nt = -(-d_out // tile)
     code = _dtype_code(X)
     stream = _stream(dev)

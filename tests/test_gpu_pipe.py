@@ -58,7 +58,9 @@ def cancelling_features(n, d, seed):
 
 @pytest.fixture
 def small_budget(monkeypatch):
-    monkeypatch.setattr(kernels, "_L2_BUDGET", 1 << 16)
+    """Below X's size for d > 75 but above one 256 B-row tile slice of the
+    40000-row graph (10.2 MB): 64-column tiles, the pipelined kernel."""
+    monkeypatch.setattr(kernels, "_L2_BUDGET", 12 << 20)
 
 
 @pytest.mark.parametrize("d", [64, 128, 200])
@@ -92,7 +94,7 @@ def test_pipe_u_mul_e_matches_oracle(small_budget, rho):
     s, dd, n = hub_graph(seed=11)
     g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
     rng = np.random.default_rng(5)
-    x = cancelling_features(n, 64, 4)
+    x = cancelling_features(n, 130, 4)  # tiled: w laid out in adjacency order, the pipe path
     w = rng.standard_normal((s.size, 1)).astype(np.float32)
     Z, _ = G.gspmm(g, kernels.mul("src", "edge"), rho, X=torch.as_tensor(x, device=DEV),
                    W=torch.as_tensor(w, device=DEV))
@@ -116,7 +118,7 @@ sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
 import paper_1909_01315_b200 as G
 from paper_1909_01315_b200 import kernels
 from test_gpu_pipe import hub_graph, cancelling_features
-kernels._L2_BUDGET = 1 << 16
+kernels._L2_BUDGET = 12 << 20
 s, d, n = hub_graph()
 g = G.from_arrays(s, d, num_nodes=n, device="cuda")
 x = torch.as_tensor(cancelling_features(n, 64, 3), device="cuda")

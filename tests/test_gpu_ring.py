@@ -31,7 +31,9 @@ def ring_on(monkeypatch):
 
 @pytest.fixture
 def small_budget(monkeypatch):
-    monkeypatch.setattr(kernels, "_L2_BUDGET", 1 << 16)
+    # below X for d >= 65 but at least one 256 B-row slice of the 6000-row
+    # graph (1.536 MB), so tiles stay 64 columns wide
+    monkeypatch.setattr(kernels, "_L2_BUDGET", 1_540_000)
 
 
 @pytest.mark.parametrize("d", [64, 65, 130, 602])

@@ -15,9 +15,13 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-@pytest.fixture
-def small_budget(monkeypatch):
-    monkeypatch.setattr(kernels, "_L2_BUDGET", 1 << 16)
+@pytest.fixture(params=["wide", "narrow"])
+def small_budget(monkeypatch, request):
+    """An L2 budget below X's size: "wide" still fits a 256 B-row tile slice
+    of the 5000-row test graph (64-column fp32 tiles, the pipelined kernel),
+    "narrow" does not (64 B-row tiles: 16 fp32 / 8 fp64 columns)."""
+    monkeypatch.setattr(kernels, "_L2_BUDGET", 1_290_000 if request.param == "wide" else (1 << 16))
+    return request.param
 
 
 def graph():
@@ -38,8 +42,9 @@ def test_tiled_copy_matches_oracle(small_budget, dtype, d, ld, rho):
     before = _lib.launch_count()
     Z, aux = G.gspmm(g, kernels.copy("src"), rho, X=X)
     launches = _lib.launch_count() - before
-    tile = 256 // base.itemsize
-    aligned = ld % tile == 0
+    tile = kernels._tile_cols(n, base.itemsize)
+    assert tile == (256 if small_budget == "wide" else 64) // base.itemsize
+    aligned = ld % tile == 0 and tile == 256 // base.itemsize
     if not aligned:
         nt = -(-d // tile)
         if dtype == np.float32 and g.to_csc().schedule().n_heavy > 0 and not kernels._RING_OFF:
