@@ -15,13 +15,11 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-@pytest.fixture(params=["wide", "narrow"])
-def small_budget(monkeypatch, request):
-    """An L2 budget below X's size: "wide" still fits a 256 B-row tile slice
-    of the 5000-row test graph (64-column fp32 tiles, the pipelined kernel),
-    "narrow" does not (64 B-row tiles: 16 fp32 / 8 fp64 columns)."""
-    monkeypatch.setattr(kernels, "_L2_BUDGET", 1_290_000 if request.param == "wide" else (1 << 16))
-    return request.param
+@pytest.fixture
+def small_budget(monkeypatch):
+    """An L2 budget below X's size (d >= 65) that still fits one 256 B-row
+    tile slice of the 5000-row test graph: 64-column fp32 tiles."""
+    monkeypatch.setattr(kernels, "_L2_BUDGET", 1_290_000)
 
 
 def graph():
@@ -42,9 +40,9 @@ def test_tiled_copy_matches_oracle(small_budget, dtype, d, ld, rho):
     before = _lib.launch_count()
     Z, aux = G.gspmm(g, kernels.copy("src"), rho, X=X)
     launches = _lib.launch_count() - before
-    tile = kernels._tile_cols(n, base.itemsize)
-    assert tile == (256 if small_budget == "wide" else 64) // base.itemsize
-    aligned = ld % tile == 0 and tile == 256 // base.itemsize
+    tile = kernels._tile_cols(n, base.itemsize, d)
+    assert tile == 256 // base.itemsize
+    aligned = ld % tile == 0
     if not aligned:
         nt = -(-d // tile)
         if dtype == np.float32 and g.to_csc().schedule().n_heavy > 0 and not kernels._RING_OFF:
@@ -149,3 +147,29 @@ def test_u_mul_e_with_windowed_gather_matches_oracle(monkeypatch, small_budget):
     want, _ = O.gspmm(s, dd, n, "mul", "src", "edge", "sum", X=x.astype(np.float64),
                       W=w.astype(np.float64))
     assert np.allclose(to_np(Z), want, rtol=RTOL32, atol=ATOL32)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("d", [20, 33, 48])
+@pytest.mark.parametrize("rho", ["sum", "mean"])
+def test_narrow_tiles_match_oracle(monkeypatch, dtype, d, rho):
+    """Rows narrower than 256 B whose slice overflows the L2 budget: 128 B /
+    64 B packed tiles (the narrow row kernel per tile), copy_u and u_mul_e."""
+    monkeypatch.setattr(kernels, "_L2_BUDGET", 1 << 16)
+    s, dd, n = graph()
+    g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
+    F = np.dtype(dtype).itemsize
+    tile = kernels._tile_cols(n, F, d)
+    assert tile * F == (64 if d * F < 256 else 256) and tile < d
+    rng = np.random.default_rng(d)
+    x = rng.standard_normal((n, d)).astype(dtype)
+    w = rng.standard_normal((s.size, 1)).astype(dtype)
+    Z, _ = G.gspmm(g, kernels.copy("src"), rho, X=torch.as_tensor(x, device=DEV))
+    want, _ = O.gspmm(s, dd, n, "copy_lhs", "src", None, rho, X=x.astype(np.float64))
+    tol = dict(rtol=RTOL32, atol=ATOL32) if dtype == np.float32 else dict(rtol=1e-12, atol=1e-12)
+    assert np.allclose(to_np(Z), want, **tol)
+    Z, _ = G.gspmm(g, kernels.mul("src", "edge"), rho, X=torch.as_tensor(x, device=DEV),
+                   W=torch.as_tensor(w, device=DEV))
+    want, _ = O.gspmm(s, dd, n, "mul", "src", "edge", rho, X=x.astype(np.float64),
+                      W=w.astype(np.float64))
+    assert np.allclose(to_np(Z), want, **tol)
