@@ -51,6 +51,9 @@ constexpr int kWarpsPerCta = 8;
 #ifndef GMP_PIPE_NB
 #define GMP_PIPE_NB 4
 #endif
+#ifndef GMP_PIPE_NB_NARROW
+#define GMP_PIPE_NB_NARROW 4
+#endif
 #ifndef GMP_ROW_MIN_BLOCKS
 #define GMP_ROW_MIN_BLOCKS 3
 #endif
@@ -573,101 +576,133 @@ __device__ __forceinline__ void spmm_accumulate(const SpmmArgs& a, int64_t pb, i
   acc.fold();
 }
 
-// Software-pipelined accumulate for the packed-tile shape: 16 feature lanes
-// per edge slot (E = 2), one float4 per lane, i.e. one 256 B tile row per
-// edge - the Reddit-shaped headline and every wide copy_u / u_mul_e sum.
-// spmm_accumulate issues a burst of U gathers, waits for all of them and
-// then runs the compensated sums, so a warp has nothing in flight while it
-// computes. Here every lane keeps a ring of NB float4 registers: step k
-// consumes ring slot k % NB and immediately refills it with the gather of
-// step k + NB (taken from the next 32-edge batch's neighbour ids near the end
-// of a batch), so NB - 1..NB gathers stay in flight through the arithmetic.
-// Same edge order per slot and the same fold points (every 2 batches = 32
-// edges per slot) as spmm_accumulate: the results are bit-identical.
-// Operands: lhs gathered by neighbour id; rhs none (copy) or a per-edge scalar
-// addressed by position or neighbour id (no edge ids needed).
-template <int OP, int MP, int NB>
+// Software-pipelined accumulate, one float4 per lane: G = 2^GL lanes per
+// edge (64 / 128 / 256 B rows for GL = 2 / 3 / 4), E = 32 / G edge slots per
+// warp step. spmm_accumulate issues a burst of U gathers, waits for all of
+// them and then runs the compensated sums, so a warp has nothing in flight
+// while it computes. Here every lane keeps a ring of NB float4 registers:
+// step t consumes ring slot t % NB and immediately refills it with the gather
+// of step t + NB (taken from the next iteration's neighbour ids near the end
+// of an iteration), so gathers stay in flight through the arithmetic.
+// An iteration covers R 32-edge index registers (R = 1 for 256 / 128 B rows,
+// 2 for 64 B rows): T = R * G steps of E edges.
+// For GL = 4 the edge order per slot and the fold points (every 32 edges per
+// slot) equal spmm_accumulate's, so the sums are bit-identical to it.
+// Operands: lhs gathered by neighbour id; rhs none (copy), a per-edge scalar
+// addressed by position or neighbour id, or the recomputed attention weight
+// (MP_AF / MP_AB) - no edge ids needed.
+// ring depth (float4 registers per lane) and index registers per iteration
+// of the pipelined accumulate, by log2 of the lanes per edge
+template <int GL>
+struct PipeR {
+  static constexpr int value = (1 << GL) >= 8 ? 1 : 8 / (1 << GL);
+};
+template <int GL>
+struct PipeNB {
+  static constexpr int value = GL >= 4 ? GMP_PIPE_NB : GMP_PIPE_NB_NARROW;
+};
+
+template <int OP, int MP, int GL, int NB>
 __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t pb, int64_t pe,
                                                      int64_t first, int64_t stride, int lane,
                                                      int slot, int col, bool valid,
                                                      const float (&rc)[3],
                                                      RowAcc<float, OP, RHO_SUM, 4>& acc) {
-  static_assert(16 % NB == 0, "ring slots must be compile-time across a batch");
+  constexpr int G = 1 << GL, E = 32 >> GL;
+  constexpr int R = G >= 8 ? 1 : 8 / G;  // 32-edge index registers per iteration
+  constexpr int T = R * G;               // steps per iteration
+  constexpr int FOLD = 32 / T > 0 ? 32 / T : 1;  // iterations per 32 edges of a slot
+  static_assert(T % NB == 0 && NB <= T, "ring slots must be compile-time across an iteration");
   constexpr bool SC = OP != OP_COPY;  // per-edge scalar rhs
-  // 32-bit offsets relative to the batch start (a row has < 2^31 edges)
+  // 32-bit offsets relative to the iteration start (a row has < 2^31 edges)
   if (pb + first >= pe) return;
   const int32_t* __restrict__ ip = a.indices + pb + first;
-  int32_t left = (int32_t)(pe - pb - first);  // edges from the current batch start on
+  int32_t left = (int32_t)(pe - pb - first);  // edges from the current iteration start on
   const int32_t step = (int32_t)stride;
   const float* lcol = static_cast<const float*>(a.lhs.data) + (valid ? col : 0);
   const uint32_t lld = a.lhs.ld * (uint32_t)sizeof(float);
   const bool r_pos = a.rhs.from_pos;
-  // lane L of a batch register holds edge 2 (L & 15) + (L >> 4) of the batch:
-  // slot s reads edge 2k + s with a width-16 shuffle from lane k (an
+  // lane L of index register q holds edge 32 q + E (L & (G-1)) + (L >> GL):
+  // slot s reads edge 32 q + E k + s with a width-G shuffle from lane k (an
   // immediate lane, no per-step lane arithmetic); the loads stay coalesced
-  const int pl = 2 * (lane & 15) + (lane >> 4);
-  // index of batch edge pl at batch offset o (0 past the row: row 0, harmless)
+  const int pl = E * (lane & (G - 1)) + (lane >> GL);
+  // index of edge pl of register q at iteration offset o (0 past the row:
+  // row 0, loaded but never summed)
   auto ld_idx = [&](int32_t o) -> int32_t { return pl + o < left ? __ldg(ip + o + pl) : 0; };
   auto ld_sc = [&](int32_t o, int32_t nb) -> float {
     if constexpr (SC) {
       if (pl + o < left) {
-        double ts = 0.0;
         const int64_t q = (ip - a.indices) + o + pl;  // CSC position
-        return rhs_scalar<float, MP>(a, r_pos ? (uint32_t)q : (uint32_t)nb, rc, ts);
+        return rhs_scalar<float, MP>(a, r_pos ? (uint32_t)q : (uint32_t)nb, rc, acc.tsum);
       }
     }
     return 0.f;
   };
   auto gather = [&](int32_t nbreg, int k) -> float4 {
-    const uint32_t r = (uint32_t)__shfl_sync(kFull, nbreg, k, 16);
+    const uint32_t r = (uint32_t)__shfl_sync(kFull, nbreg, k, G);
     return __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(lcol) +
                                                  (uint64_t)r * lld));
   };
-  int32_t cur = ld_idx(0);
-  int32_t nxt = ld_idx(step);
-  float wcur = ld_sc(0, cur);
+  int32_t cur[R], nxt[R];
+  float wcur[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    cur[q] = ld_idx(32 * q);
+    nxt[q] = ld_idx(step + 32 * q);
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) wcur[q] = ld_sc(32 * q, cur[q]);
   float4 buf[NB];
 #pragma unroll
-  for (int k = 0; k < NB; ++k) buf[k] = gather(cur, k);
+  for (int t = 0; t < NB; ++t) buf[t] = gather(cur[t / G], t % G);
 
   for (int b = 0;; ++b) {
-    const int32_t nn = ld_idx(2 * step);
-    const float wnxt = ld_sc(step, nxt);
+    int32_t nn[R];
+    float wnxt[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) nn[q] = ld_idx(2 * step + 32 * q);
+#pragma unroll
+    for (int q = 0; q < R; ++q) wnxt[q] = ld_sc(step + 32 * q, nxt[q]);
     auto steps = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const bool use = FULL || 2 * k + slot < left;
-        const float4 x = buf[k % NB];
+      for (int t = 0; t < T; ++t) {
+        const int q = t / G, k = t % G;
+        const bool use = FULL || 32 * q + E * k + slot < left;
+        const float4 x = buf[t % NB];
         float va[4] = {x.x, x.y, x.z, x.w};
         float vb[4] = {0.f, 0.f, 0.f, 0.f};
         if constexpr (SC) {
-          const float w = __shfl_sync(kFull, wcur, k, 16);
+          const float w = __shfl_sync(kFull, wcur[q], k, G);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) vb[q] = w;
+          for (int c = 0; c < 4; ++c) vb[c] = w;
         }
         if constexpr (!FULL) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            va[q] = use ? va[q] : 0.f;
-            vb[q] = use ? vb[q] : 0.f;
+          for (int c = 0; c < 4; ++c) {
+            va[c] = use ? va[c] : 0.f;
+            vb[c] = use ? vb[c] : 0.f;
           }
         }
-        // refill this ring slot with step k + NB (the next batch's ids near
-        // the end; past the last batch they are 0: row 0, never used)
-        buf[k % NB] = k + NB < 16 ? gather(cur, k + NB) : gather(nxt, k + NB - 16);
+        // refill this ring slot with step t + NB (the next iteration's ids
+        // near the end; past the last iteration they are 0: row 0, unused)
+        const int tn = t + NB;
+        buf[t % NB] = tn < T ? gather(cur[tn / G], tn % G) : gather(nxt[(tn - T) / G], (tn - T) % G);
         acc.add(va, vb, true, 0);
       }
     };
-    if (left >= 32) steps(std::true_type{});
+    if (left >= 32 * R) steps(std::true_type{});
     else steps(std::false_type{});
-    if (b & 1) acc.fold();
+    if ((b + 1) % FOLD == 0) acc.fold();
     left -= step;
     if (left <= 0) break;
     ip += step;
-    cur = nxt;
-    nxt = nn;
-    wcur = wnxt;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      cur[q] = nxt[q];
+      nxt[q] = nn[q];
+      wcur[q] = wnxt[q];
+    }
   }
   acc.fold();
 }
@@ -948,8 +983,8 @@ struct Unroll {
 // share a warp and longer rows stage edge ids in shared memory. Wide kernels
 // (every d >= 16 with V=4, and all fp64 launches) compile without those paths
 // so their main loop is scheduled on its own.
-template <typename T, int OP, int RHO, int V, int MP, bool NARROW, bool PIPE = false>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, PIPE ? GMP_PIPE_MIN_BLOCKS : GMP_ROW_MIN_BLOCKS)
+template <typename T, int OP, int RHO, int V, int MP, bool NARROW, int PGL = 0>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, PGL ? GMP_PIPE_MIN_BLOCKS : GMP_ROW_MIN_BLOCKS)
 spmm_rows_kernel(const SpmmArgs a) {
   using Acc = RowAcc<T, OP, RHO, V>;
   using ExtT = typename Acc::ExtT;
@@ -981,8 +1016,9 @@ spmm_rows_kernel(const SpmmArgs a) {
   const int64_t heavy_blocks = a.n_heavy * ncl;
   const bool heavy = local < heavy_blocks;  // block-uniform
   const int crank = heavy ? (int)(local % ncl) : 0;
-  // light rows share a warp, one per lane group (NARROW kernels; the PIPE
-  // kernel's two 16-lane slots take one light row each)
+  // light rows share a warp, one per lane group (NARROW kernels and the
+  // pipelined ones: PGL = log2 of the lanes per edge)
+  constexpr bool PIPE = PGL != 0;
   const bool light = (NARROW || PIPE) && local >= heavy_blocks + a.medium_blocks;  // block-uniform
 
   int64_t row;
@@ -1045,6 +1081,9 @@ spmm_rows_kernel(const SpmmArgs a) {
     if (light) {
       spmm_accumulate_slot<T, OP, RHO, V, MP, GMP_PIPE_NB>(a, pb, pe, col, valid, ha, hb, rc, acc);
       if (row < 0) return;
+      if constexpr (MP == MP_AB) {
+        if (a.attn_t && tile == 0 && gl == 0) a.attn_t[row] = acc.tsum;
+      }
       if (a.counts && tile == 0 && gl == 0) a.counts[row] = deg;
       write_row<T, OP, RHO, V>(a, row, deg, col, valid, acc);
       return;
@@ -1078,17 +1117,17 @@ spmm_rows_kernel(const SpmmArgs a) {
     // nothing to accumulate
   } else if (heavy) {
     if constexpr (PIPE)
-      spmm_accumulate_pipe<OP, MP, GMP_PIPE_NB>(a, pb, pe,
-                                                ((int64_t)crank * kWarpsPerCta + warp) * 32,
-                                                (int64_t)32 * kWarpsPerCta * ncl, lane, slot, col,
-                                                valid, rc, acc);
+      spmm_accumulate_pipe<OP, MP, PGL, PipeNB<PGL>::value>(
+          a, pb, pe, ((int64_t)crank * kWarpsPerCta + warp) * 32 * PipeR<PGL>::value,
+          (int64_t)32 * PipeR<PGL>::value * kWarpsPerCta * ncl, lane, slot, col, valid, rc, acc);
     else
       spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, ((int64_t)crank * kWarpsPerCta + warp) * 32,
                                             (int64_t)32 * kWarpsPerCta * ncl, lane, slot, E, col,
                                             valid, ha, hb, rc, acc);
   } else {
     if constexpr (PIPE)
-      spmm_accumulate_pipe<OP, MP, GMP_PIPE_NB>(a, pb, pe, 0, 32, lane, slot, col, valid, rc, acc);
+      spmm_accumulate_pipe<OP, MP, PGL, PipeNB<PGL>::value>(a, pb, pe, 0, 32 * PipeR<PGL>::value,
+                                                             lane, slot, col, valid, rc, acc);
     else
       spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, 0, 32, lane, slot, E, col, valid, ha, hb,
                                             rc, acc);
@@ -1231,21 +1270,29 @@ cudaError_t launch_rows_cfg(Kern kern, const SpmmArgs& a, int64_t grid, size_t s
 }
 
 // fp32 launches that take the pipelined gather ring (spmm_accumulate_pipe):
-// sum / mean of copy_u or u_mul_e (per-edge scalar) with one 256 B tile row
-// per edge (16 lanes x float4) and no edge ids. The host sizes the grid by
-// the same predicate (light rows two per warp). GMP_NO_PIPE=1 disables it.
+// sum / mean of copy_u, u_mul_e (per-edge scalar) or the fused GAT attention
+// (MP_AF / MP_AB) with one float4 per lane and 4, 8 or 16 lanes per edge
+// (64 / 128 / 256 B rows), no edge ids. The host sizes the grid by the same
+// predicate (light rows several per warp). GMP_NO_PIPE=1 disables it.
 inline bool pipe_launch(int V, int rho, int op, int mp, int g_log2, int need_eid) {
   static const bool off = getenv("GMP_NO_PIPE") != nullptr;
-  return !off && V == 4 && rho == RHO_SUM && g_log2 == 4 && !need_eid &&
-         ((op == OP_COPY && mp == MP_F) || (op == OP_MUL && mp == MP_FS));
+  return !off && V == 4 && rho == RHO_SUM && g_log2 >= 2 && g_log2 <= 4 && !need_eid &&
+         ((op == OP_COPY && mp == MP_F) ||
+          (op == OP_MUL && (mp == MP_FS || mp == MP_AF || mp == MP_AB)));
 }
 
 template <typename T, int OP, int RHO, int V, int MP>
 cudaError_t launch_spmm_rows_t(const SpmmArgs& a, int64_t grid, cudaStream_t s) {
   if constexpr (sizeof(T) == 4 && V == 4 && RHO == RHO_SUM &&
-                ((OP == OP_COPY && MP == MP_F) || (OP == OP_MUL && MP == MP_FS))) {
-    if (pipe_launch(V, RHO, OP, MP, a.g_log2, a.need_eid))
-      return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false, true>, a, grid, 0, s);
+                ((OP == OP_COPY && MP == MP_F) ||
+                 (OP == OP_MUL && (MP == MP_FS || MP == MP_AF || MP == MP_AB)))) {
+    if (pipe_launch(V, RHO, OP, MP, a.g_log2, a.need_eid)) {
+      if (a.g_log2 == 4)
+        return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false, 4>, a, grid, 0, s);
+      if (a.g_log2 == 3)
+        return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false, 3>, a, grid, 0, s);
+      return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false, 2>, a, grid, 0, s);
+    }
   }
   if constexpr (sizeof(T) == 4) {
     if (narrow_launch<V>(a.g_log2))

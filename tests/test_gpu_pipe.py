@@ -1,5 +1,7 @@
-"""Pipelined gather ring of the packed-tile g-SpMM (spmm_accumulate_pipe,
-spmm_rows.cuh): copy_u / u_mul_e + sum/mean over 256 B tile rows, heavy rows
+"""Pipelined gather ring of the row g-SpMM (spmm_accumulate_pipe,
+spmm_rows.cuh): copy_u / u_mul_e + sum/mean over 64 / 128 / 256 B rows (4 /
+8 / 16 lanes per edge; the fused GAT modes are covered by
+test_gpu_gat_fused.py), heavy rows
 (one CTA), medium rows (one warp) and light rows (two per warp) - against the
 oracle at the fp32 bar, including a hub row whose exact sum cancels (a plain
 fp32 accumulation misses the bar there by orders of magnitude), ragged last
@@ -63,7 +65,7 @@ def small_budget(monkeypatch):
     monkeypatch.setattr(kernels, "_L2_BUDGET", 12 << 20)
 
 
-@pytest.mark.parametrize("d", [64, 128, 200])
+@pytest.mark.parametrize("d", [16, 32, 64, 128, 200])  # 4 / 8 / 16 lanes per edge
 @pytest.mark.parametrize("rho", ["sum", "mean"])
 def test_pipe_copy_matches_oracle(small_budget, d, rho):
     s, dd, n = hub_graph()
@@ -74,16 +76,17 @@ def test_pipe_copy_matches_oracle(small_budget, d, rho):
     assert_close32(to_np(Z), want)
 
 
-def test_pipe_exact_under_cancellation(small_budget):
+@pytest.mark.parametrize("d", [16, 32, 64])
+def test_pipe_exact_under_cancellation(small_budget, d):
     s, dd, n = hub_graph()
     g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
-    x = cancelling_features(n, 64, 3)
+    x = cancelling_features(n, d, 3)
     Z, _ = G.gspmm(g, kernels.copy("src"), "sum", X=torch.as_tensor(x, device=DEV))
     want, _ = O.gspmm(s, dd, n, "copy_lhs", "src", None, "sum", X=x.astype(np.float64))
     assert_close32(to_np(Z), want)
     # the bar is meaningful here: a plain fp32 sum of the hub row misses it
     hub = np.flatnonzero(dd == 0)
-    naive = np.zeros(64, dtype=np.float32)
+    naive = np.zeros(d, dtype=np.float32)
     for u in s[hub]:
         naive += x[u]
     assert not np.allclose(naive, want[0], rtol=1e-5, atol=1e-6)
