@@ -602,21 +602,23 @@ struct PipeNB {
   static constexpr int value = GL >= 4 ? GMP_PIPE_NB : GMP_PIPE_NB_NARROW;
 };
 
-template <int OP, int MP, int GL, int NB>
+template <int OP, int RHO, int MP, int GL, int NB>
 __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t pb, int64_t pe,
                                                      int64_t first, int64_t stride, int lane,
                                                      int slot, int col, bool valid,
                                                      const float (&rc)[3],
-                                                     RowAcc<float, OP, RHO_SUM, 4>& acc) {
+                                                     RowAcc<float, OP, RHO, 4>& acc) {
   constexpr int G = 1 << GL, E = 32 >> GL;
   constexpr int R = G >= 8 ? 1 : 8 / G;  // 32-edge index registers per iteration
   constexpr int T = R * G;               // steps per iteration
   constexpr int FOLD = 32 / T > 0 ? 32 / T : 1;  // iterations per 32 edges of a slot
   static_assert(T % NB == 0 && NB <= T, "ring slots must be compile-time across an iteration");
   constexpr bool SC = OP != OP_COPY;  // per-edge scalar rhs
+  constexpr bool EXT = RHO != RHO_SUM;  // max / min: edge ids for the arg
   // 32-bit offsets relative to the iteration start (a row has < 2^31 edges)
   if (pb + first >= pe) return;
   const int32_t* __restrict__ ip = a.indices + pb + first;
+  const int32_t* __restrict__ ep = a.eids + pb + first;
   int32_t left = (int32_t)(pe - pb - first);  // edges from the current iteration start on
   const int32_t step = (int32_t)stride;
   const float* lcol = static_cast<const float*>(a.lhs.data) + (valid ? col : 0);
@@ -629,6 +631,10 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
   // index of edge pl of register q at iteration offset o (0 past the row:
   // row 0, loaded but never summed)
   auto ld_idx = [&](int32_t o) -> int32_t { return pl + o < left ? __ldg(ip + o + pl) : 0; };
+  auto ld_eid = [&](int32_t o) -> int32_t {
+    if constexpr (EXT) return pl + o < left ? __ldg(ep + o + pl) : 0;
+    return 0;
+  };
   auto ld_sc = [&](int32_t o, int32_t nb) -> float {
     if constexpr (SC) {
       if (pl + o < left) {
@@ -643,12 +649,14 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
     return __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(lcol) +
                                                  (uint64_t)r * lld));
   };
-  int32_t cur[R], nxt[R];
+  int32_t cur[R], nxt[R], ecur[R], enxt[R];
   float wcur[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     cur[q] = ld_idx(32 * q);
     nxt[q] = ld_idx(step + 32 * q);
+    ecur[q] = ld_eid(32 * q);
+    enxt[q] = ld_eid(step + 32 * q);
   }
 #pragma unroll
   for (int q = 0; q < R; ++q) wcur[q] = ld_sc(32 * q, cur[q]);
@@ -657,10 +665,13 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
   for (int t = 0; t < NB; ++t) buf[t] = gather(cur[t / G], t % G);
 
   for (int b = 0;; ++b) {
-    int32_t nn[R];
+    int32_t nn[R], enn[R];
     float wnxt[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) nn[q] = ld_idx(2 * step + 32 * q);
+    for (int q = 0; q < R; ++q) {
+      nn[q] = ld_idx(2 * step + 32 * q);
+      enn[q] = ld_eid(2 * step + 32 * q);
+    }
 #pragma unroll
     for (int q = 0; q < R; ++q) wnxt[q] = ld_sc(step + 32 * q, nxt[q]);
     auto steps = [&](auto full_tag) {
@@ -677,18 +688,19 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
 #pragma unroll
           for (int c = 0; c < 4; ++c) vb[c] = w;
         }
-        if constexpr (!FULL) {
+        if constexpr (!FULL && !EXT) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             va[c] = use ? va[c] : 0.f;
             vb[c] = use ? vb[c] : 0.f;
           }
         }
+        const int32_t e = EXT ? __shfl_sync(kFull, ecur[q], k, G) : 0;
         // refill this ring slot with step t + NB (the next iteration's ids
         // near the end; past the last iteration they are 0: row 0, unused)
         const int tn = t + NB;
         buf[t % NB] = tn < T ? gather(cur[tn / G], tn % G) : gather(nxt[(tn - T) / G], (tn - T) % G);
-        acc.add(va, vb, true, 0);
+        acc.add(va, vb, use, e);  // extrema: masked edges excluded by `use`
       }
     };
     if (left >= 32 * R) steps(std::true_type{});
@@ -697,10 +709,13 @@ __device__ __forceinline__ void spmm_accumulate_pipe(const SpmmArgs& a, int64_t 
     left -= step;
     if (left <= 0) break;
     ip += step;
+    ep += step;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       cur[q] = nxt[q];
       nxt[q] = nn[q];
+      ecur[q] = enxt[q];
+      enxt[q] = enn[q];
       wcur[q] = wnxt[q];
     }
   }
@@ -1117,7 +1132,7 @@ spmm_rows_kernel(const SpmmArgs a) {
     // nothing to accumulate
   } else if (heavy) {
     if constexpr (PIPE)
-      spmm_accumulate_pipe<OP, MP, PGL, PipeNB<PGL>::value>(
+      spmm_accumulate_pipe<OP, RHO, MP, PGL, PipeNB<PGL>::value>(
           a, pb, pe, ((int64_t)crank * kWarpsPerCta + warp) * 32 * PipeR<PGL>::value,
           (int64_t)32 * PipeR<PGL>::value * kWarpsPerCta * ncl, lane, slot, col, valid, rc, acc);
     else
@@ -1126,7 +1141,7 @@ spmm_rows_kernel(const SpmmArgs a) {
                                             valid, ha, hb, rc, acc);
   } else {
     if constexpr (PIPE)
-      spmm_accumulate_pipe<OP, MP, PGL, PipeNB<PGL>::value>(a, pb, pe, 0, 32 * PipeR<PGL>::value,
+      spmm_accumulate_pipe<OP, RHO, MP, PGL, PipeNB<PGL>::value>(a, pb, pe, 0, 32 * PipeR<PGL>::value,
                                                              lane, slot, col, valid, rc, acc);
     else
       spmm_accumulate<T, OP, RHO, V, MP, U>(a, pb, pe, 0, 32, lane, slot, E, col, valid, ha, hb,
@@ -1276,16 +1291,19 @@ cudaError_t launch_rows_cfg(Kern kern, const SpmmArgs& a, int64_t grid, size_t s
 // predicate (light rows several per warp). GMP_NO_PIPE=1 disables it.
 inline bool pipe_launch(int V, int rho, int op, int mp, int g_log2, int need_eid) {
   static const bool off = getenv("GMP_NO_PIPE") != nullptr;
-  return !off && V == 4 && rho == RHO_SUM && g_log2 >= 2 && g_log2 <= 4 && !need_eid &&
-         ((op == OP_COPY && mp == MP_F) ||
-          (op == OP_MUL && (mp == MP_FS || mp == MP_AF || mp == MP_AB)));
+  if (off || V != 4 || g_log2 < 2 || g_log2 > 4) return false;
+  if (rho != RHO_SUM)  // max / min of copy_u: edge ids only for the arg
+    return op == OP_COPY && mp == MP_F;
+  return !need_eid && ((op == OP_COPY && mp == MP_F) ||
+                       (op == OP_MUL && (mp == MP_FS || mp == MP_AF || mp == MP_AB)));
 }
 
 template <typename T, int OP, int RHO, int V, int MP>
 cudaError_t launch_spmm_rows_t(const SpmmArgs& a, int64_t grid, cudaStream_t s) {
-  if constexpr (sizeof(T) == 4 && V == 4 && RHO == RHO_SUM &&
+  if constexpr (sizeof(T) == 4 && V == 4 &&
                 ((OP == OP_COPY && MP == MP_F) ||
-                 (OP == OP_MUL && (MP == MP_FS || MP == MP_AF || MP == MP_AB)))) {
+                 (RHO == RHO_SUM && OP == OP_MUL &&
+                  (MP == MP_FS || MP == MP_AF || MP == MP_AB)))) {
     if (pipe_launch(V, RHO, OP, MP, a.g_log2, a.need_eid)) {
       if (a.g_log2 == 4)
         return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false, 4>, a, grid, 0, s);

@@ -146,3 +146,19 @@ def test_pipe_equals_burst_kernel_on_heavy_and_medium_rows(tmp_path):
     want, _ = O.gspmm(s, dd, n, "copy_lhs", "src", None, "sum",
                       X=cancelling_features(n, 64, 3).astype(np.float64))
     assert_close32(outs["burst"], want)
+
+
+@pytest.mark.parametrize("d", [16, 32, 64])
+@pytest.mark.parametrize("rho", ["max", "min"])
+def test_pipe_extrema_bit_exact(small_budget, d, rho):
+    """max / min of copy_u through the pipelined ring: values and arg edges
+    (smallest edge id among ties) equal the reference's bit for bit, with
+    many exact ties (values drawn from 7 levels)."""
+    s, dd, n = hub_graph(seed=13)
+    g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
+    rng = np.random.default_rng(d)
+    x = rng.integers(-3, 4, size=(n, d)).astype(np.float32) * np.float32(0.5)
+    Z, aux = G.gspmm(g, kernels.copy("src"), rho, X=torch.as_tensor(x, device=DEV))
+    want, warg = O.gspmm(s, dd, n, "copy_lhs", "src", None, rho, X=x.astype(np.float64))
+    assert np.array_equal(to_np(Z), want.astype(np.float32))
+    assert np.array_equal(to_np(aux.arg_edge), warg)
