@@ -171,6 +171,19 @@ int pick_v(size_t F, int width, const Opnd* ops, int nops, const void* out, int6
   return 1;
 }
 
+// every full-width operand's rows are 16 B aligned runs of whole float4s
+// (ld % 4 == 0, 16 B-aligned base), so 16 B gathers stay in bounds of the row
+// even past a width that is not a multiple of 4
+bool gathers_v4(const Opnd* ops, int nops) {
+  bool any = false;
+  for (int i = 0; i < nops; ++i) {
+    if (!ops[i].present || ops[i].dev.bcast) continue;
+    if (ops[i].dev.ld % 4 != 0 || !aligned(ops[i].dev.data, 16)) return false;
+    any = true;
+  }
+  return any;
+}
+
 // Validate phi's operands and derive d_out (kernels.py:224-252).
 int check_operands(int op, const gmp_operand* lhs, const gmp_operand* rhs, int32_t* d_out_expected) {
   if (op < GMP_COPY_LHS || op > GMP_DOT) return fail(GMP_EINVAL, "unknown op %d", op);
@@ -413,13 +426,21 @@ static int gspmm_impl(const gmp_adj* adj, const gmp_sched* sched, int op, int rh
   }
 
   int V = pick_v(F, d_out, ops, 2, Z, ldz, ext ? arg : nullptr);
-  // sum / mean into an output whose rows are only 8 B aligned (a column tile
-  // of a row-major Z): keep 16 B gathers, store each 4-vector as two halves
   int z_split = 0;
-  if (!ext && V < 4 && F == 4 && ldz % 2 == 0 && aligned(Z, 8) &&
-      pick_v(F, d_out, ops, 2, nullptr, 0, nullptr) == 4) {
-    V = 4;
-    z_split = 1;
+  if (!ext && V < 4 && F == 4) {
+    if (ldz % 2 == 0 && aligned(Z, 8) && pick_v(F, d_out, ops, 2, nullptr, 0, nullptr) == 4) {
+      // sum / mean into an output whose rows are only 8 B aligned (a column
+      // tile of a row-major Z): keep 16 B gathers, store each 4-vector as two
+      // 8 B halves
+      V = 4;
+      z_split = 1;
+    } else if (d_out % 4 && gathers_v4(ops, 2)) {
+      // a width that is not a multiple of 4 over 16 B-aligned operand rows
+      // (a padded projection, the last packed column tile): 16 B gathers, the
+      // last vector of a row stored element by element
+      V = 4;
+      z_split = (ldz % 4 == 0 && aligned(Z, 16)) ? 0 : ((ldz % 2 == 0 && aligned(Z, 8)) ? 1 : 2);
+    }
   }
   const bool src_full = (ops[0].dev.target == GMP_SRC && !ops[0].dev.bcast) ||
                         (ops[1].present && ops[1].dev.target == GMP_SRC && !ops[1].dev.bcast);
@@ -887,7 +908,13 @@ int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int
   Opnd ops[2] = {};
   ops[0].present = true; ops[0].dev.data = X; ops[0].dev.ld = ldx; ops[0].dev.dim = d;
   ops[0].dev.target = GMP_SRC;
-  const int V = pick_v(F, d, ops, 1, Z, ldz, nullptr);
+  int V = pick_v(F, d, ops, 1, Z, ldz, nullptr);
+  int z_split = 0;
+  if (V < 4 && F == 4 && d % 4 && gathers_v4(ops, 1)) {
+    // padded rows (ld a multiple of 4): 16 B gathers, tail-masked stores
+    V = 4;
+    z_split = (ldz % 4 == 0 && aligned(Z, 16)) ? 0 : ((ldz % 2 == 0 && aligned(Z, 8)) ? 1 : 2);
+  }
   const int tw = pick_tile(tuning, d, V, F, adj->n_rows, true, 32 * V);
   const int G = std::min(32, next_pow2((tw + V - 1) / V));
   const int ntiles = (d + tw - 1) / tw;
@@ -908,6 +935,7 @@ int gmp_gat_aggregate(const gmp_adj* adj, const gmp_sched* sched, int dtype, int
   a.indptr = adj->indptr; a.indices = adj->indices; a.eids = adj->eids; a.order = order;
   a.n_rows = adj->n_rows; a.n_heavy = n_heavy; a.n_medium = n_medium;
   a.medium_blocks = medium_blocks; a.blocks_per_tile = bpt_rows;
+  a.z_split = z_split;
   a.d_out = d; a.tile_cols = tw; a.g_log2 = log2i(G); a.mean = 0;
   a.lhs = row_operand(ops[0]);
   a.rhs.data = backward ? pack : el; a.rhs.ld = 1; a.rhs.mode = M_SCALAR;

@@ -113,7 +113,8 @@ struct SpmmArgs {
   const void* attn_pack;  // (n, PackW<T>) 32 B rows [er, max, inv_sum, w (, w_lo)]
   double* attn_t;         // MP_AB: t[u] = sum_{u->v} alpha_e w[v] (nullable)
   int32_t cluster;        // CTAs per heavy row (a thread-block cluster), 1 = one CTA
-  int32_t z_split;        // Z rows only 8 B aligned: store a 4-vector as two 8 B halves
+  int32_t z_split;        // 1: Z rows only 8 B aligned: store a 4-vector as two 8 B halves;
+                          // 2: 4 B aligned: element stores
   // fp64 row sums (sum / mean only; null acc64: plain store of Z). acc_mode
   // bits: kAccRead - add acc64[row] first (staged sums over several edge
   // blocks of the same rows, gmp_gspmm_staged); kAccZ - round once into Z
@@ -945,6 +946,9 @@ __device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_
   T* z = static_cast<T*>(a.Z) + row * a.ldz;
   T out[V];
   if constexpr (RHO == RHO_SUM) {
+    // columns of this lane's vector inside the output: < V only for the last
+    // vector of a width that is not a multiple of V (tail-masked float4s)
+    const int nv = min(V, a.d_out - col);
     int64_t dg = deg;
     double vs[V];
 #pragma unroll
@@ -953,11 +957,13 @@ __device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_
       double* ap = a.acc64 + row * a.ldacc + col;
       if (a.acc_mode & kAccRead) {
 #pragma unroll
-        for (int k = 0; k < V; ++k) vs[k] += ap[k];
+        for (int k = 0; k < V; ++k)
+          if (k < nv) vs[k] += ap[k];
       }
       if (a.acc_mode & kAccStore) {
 #pragma unroll
-        for (int k = 0; k < V; ++k) ap[k] = vs[k];
+        for (int k = 0; k < V; ++k)
+          if (k < nv) ap[k] = vs[k];
       }
       if (!(a.acc_mode & kAccZ)) return;
       if (a.deg_full) dg = a.deg_full[row];
@@ -967,6 +973,12 @@ __device__ __forceinline__ void write_row(const SpmmArgs& a, int64_t row, int64_
       double v = vs[k];
       if (a.mean && dg > 0) v = v / (double)dg;  // kernels.py:719-722
       out[k] = (T)v;
+    }
+    if (nv < V || a.z_split == 2) {  // element stores (tail, or 4 B-aligned rows)
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (k < nv) z[col + k] = out[k];
+      return;
     }
     if constexpr (V == 4) {
       if (a.z_split) {  // e.g. a 64-column tile written straight into Z with ld 602

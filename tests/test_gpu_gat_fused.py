@@ -70,7 +70,8 @@ def oracle_grads(s, d, n, el, er, X, shared, dout):
 
 
 @pytest.mark.parametrize("shared,H,dh", [(False, 1, 16), (False, 3, 8), (True, 2, 5),
-                                         (False, 1, 1), (False, 2, 70), (True, 1, 130)])
+                                         (False, 1, 1), (False, 2, 70), (True, 1, 130),
+                                         (False, 1, 41), (True, 1, 21)])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_fused_gat_matches_oracle(shared, H, dh, dtype):
     s, d, n = hub_graph()

@@ -173,3 +173,35 @@ def test_narrow_tiles_match_oracle(monkeypatch, dtype, d, rho):
     want, _ = O.gspmm(s, dd, n, "mul", "src", "edge", rho, X=x.astype(np.float64),
                       W=w.astype(np.float64))
     assert np.allclose(to_np(Z), want, **tol)
+
+
+@pytest.mark.parametrize("d", [9, 21, 41, 43])
+@pytest.mark.parametrize("rho", ["sum", "mean"])
+def test_odd_width_rows_match_oracle(d, rho):
+    """Widths that are not a multiple of 4 gather float4s from zero-padded
+    rows and store the last vector of a row element by element."""
+    s, dd, n = graph()
+    g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
+    rng = np.random.default_rng(d)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    w = rng.standard_normal((s.size, 1)).astype(np.float32)
+    Z, _ = G.gspmm(g, kernels.copy("src"), rho, X=torch.as_tensor(x, device=DEV))
+    assert Z.shape == (n, d)
+    want, _ = O.gspmm(s, dd, n, "copy_lhs", "src", None, rho, X=x.astype(np.float64))
+    assert np.allclose(to_np(Z), want, rtol=RTOL32, atol=ATOL32)
+    Z, _ = G.gspmm(g, kernels.mul("src", "edge"), rho, X=torch.as_tensor(x, device=DEV),
+                   W=torch.as_tensor(w, device=DEV))
+    want, _ = O.gspmm(s, dd, n, "mul", "src", "edge", rho, X=x.astype(np.float64),
+                      W=w.astype(np.float64))
+    assert np.allclose(to_np(Z), want, rtol=RTOL32, atol=ATOL32)
+
+
+def test_last_packed_tile_tail_columns(small_budget):
+    """d = 602: the last 256 B packed tile holds 26 columns (6 float4s + 2);
+    its Z columns are written in place into rows with ld 602."""
+    s, dd, n = graph()
+    g = G.from_arrays(s, dd, num_nodes=n, device=DEV)
+    x = np.random.default_rng(3).standard_normal((n, 602)).astype(np.float32)
+    Z, _ = G.gspmm(g, kernels.copy("src"), "sum", X=torch.as_tensor(x, device=DEV))
+    want, _ = O.gspmm(s, dd, n, "copy_lhs", "src", None, "sum", X=x.astype(np.float64))
+    assert np.allclose(to_np(Z), want, rtol=RTOL32, atol=ATOL32)
