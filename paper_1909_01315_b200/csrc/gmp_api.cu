@@ -769,6 +769,24 @@ static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sche
       e = launch_edge_softmax_slots(F == 8, V, bwd, uv, sl, st);
       g_launches++;
     }
+  } else if (sched && sched->order && ntiles == 1) {
+    // rows [0, n_medium) of the schedule: CTA / warp per row; the short rows
+    // after them one per lane group; empty rows are not launched
+    const int64_t n_med = std::max(n_heavy, std::min(sched->n_medium, sched->n_nonempty));
+    SoftmaxArgs hm = a;
+    hm.n_rows = n_med;
+    hm.blocks_per_tile = n_heavy + (n_med - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;
+    e = hm.blocks_per_tile > 0 ? launch_edge_softmax(F == 8, V, bwd, uv, hm, hm.blocks_per_tile, st)
+                               : cudaSuccess;
+    g_launches++;
+    SoftmaxArgs sl = a;
+    sl.order = a.order + n_med;
+    sl.n_rows = sched->n_nonempty - n_med;
+    sl.n_heavy = 0;
+    if (e == cudaSuccess && sl.n_rows > 0) {
+      e = launch_edge_softmax_slots(F == 8, V, bwd, uv, sl, st);
+      g_launches++;
+    }
   } else {
     e = launch_edge_softmax(F == 8, V, bwd, uv, a, a.blocks_per_tile * ntiles, st);
     g_launches++;
