@@ -68,7 +68,11 @@ typedef struct {
  * given, edge-keyed passes over heavy rows (edge_softmax statistics) run in
  * L2-sized edge-id windows. When the largest row holds more than half of one
  * SM's share of the edges, heavy rows are reduced by a cluster of 8 CTAs
- * (partials merged through distributed shared memory, in rank order). */
+ * (partials merged through distributed shared memory, in rank order).
+ * segplan (nullable): the window-major piece layout of the heavy rows'
+ * in-edges (gmp_segplan below); when given, the edge_softmax statistics of
+ * the heavy rows run as one chunked segmented pass over it. */
+typedef struct gmp_segplan gmp_segplan;
 typedef struct {
   const int32_t* order;
   int64_t n_heavy;
@@ -78,7 +82,39 @@ typedef struct {
   int32_t light_threshold;
   const int32_t* sorted_eids;
   int64_t max_degree;      /* largest row degree (set by gmp_build_schedule) */
+  const gmp_segplan* segplan;
 } gmp_sched;
+
+/* Window-major layout of the heavy rows' in-edges for the segmented
+ * edge_softmax statistics (built once per graph, window and lane-group
+ * count by the host, kernels._softmax_segplan). Replaces the reference's
+ * per-destination walk of the in-adjacency (kernels.py:340-466 _GroupedWalk
+ * under messaging.py:105-126) for the rows order[0..n_heavy) of the schedule:
+ *   perm       n_pos entries: those rows' in-edge ids ordered by
+ *              (eid / win, heavy row index r, eid), each (window, row)
+ *              segment padded with -1 to a multiple of `group` positions
+ *              (the lane groups of one warp sub-step: 32 / next_pow2(H / V));
+ *   sub-steps  runs of `group` positions; pieces = the segments cut every
+ *              GMP_SEG_CHUNK_SUB sub-steps (a chunk); piece ids ascend;
+ *   starts     ceil(n_pos / group / 32) words, bit j set = sub-step j
+ *              starts a piece;
+ *   chunk_piece  one per chunk: the piece id of its first sub-step;
+ *   row_ptr    n_heavy + 1, row_pieces n_pieces: the piece ids of heavy
+ *              row r, ascending (window order).
+ * win is sized so the score rows of about one window stay L2-resident. A
+ * plan whose group does not match the launch's lane layout is ignored. */
+#define GMP_SEG_CHUNK_SUB 16
+struct gmp_segplan {
+  int64_t n_pos;
+  int64_t n_pieces;
+  int64_t win;
+  int64_t group;
+  const int32_t* perm;
+  const uint32_t* starts;
+  const int32_t* chunk_piece;
+  const int64_t* row_ptr;
+  const int32_t* row_pieces;
+};
 
 /* COO edge list in edge-id order (graph.py:98-100). */
 typedef struct {

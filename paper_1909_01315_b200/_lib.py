@@ -41,7 +41,16 @@ class GmpSched(ctypes.Structure):
     _fields_ = [("order", ctypes.c_void_p), ("n_heavy", ctypes.c_int64),
                 ("n_medium", ctypes.c_int64), ("n_nonempty", ctypes.c_int64),
                 ("heavy_threshold", ctypes.c_int32), ("light_threshold", ctypes.c_int32),
-                ("sorted_eids", ctypes.c_void_p), ("max_degree", ctypes.c_int64)]
+                ("sorted_eids", ctypes.c_void_p), ("max_degree", ctypes.c_int64),
+                ("segplan", ctypes.c_void_p)]
+
+
+class GmpSegplan(ctypes.Structure):
+    _fields_ = [("n_pos", ctypes.c_int64), ("n_pieces", ctypes.c_int64), ("win", ctypes.c_int64),
+                ("group", ctypes.c_int64),
+                ("perm", ctypes.c_void_p), ("starts", ctypes.c_void_p),
+                ("chunk_piece", ctypes.c_void_p), ("row_ptr", ctypes.c_void_p),
+                ("row_pieces", ctypes.c_void_p)]
 
 
 class GmpCoo(ctypes.Structure):

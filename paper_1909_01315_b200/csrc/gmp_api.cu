@@ -689,10 +689,35 @@ static int softmax_vec(size_t F, int32_t H) {
   return 1;
 }
 
+static_assert(GMP_SEG_CHUNK_SUB == kSegChunkSub, "gmp.h and softmax.cuh disagree on the chunk");
+
+// Segmented statistics layout in the workspace: [stats | counter | pm | pl]
+struct SegLayout {
+  bool on;
+  size_t off_counter, off_pm, off_pl, bytes;
+};
+
+static SegLayout seg_layout(const gmp_adj* adj, const gmp_sched* sched, int32_t H, size_t F) {
+  SegLayout p{};
+  p.bytes = gmp_edge_softmax_workspace_size(adj ? adj->n_rows : 0, H);
+  const gmp_segplan* sp = sched ? sched->segplan : nullptr;
+  if (!adj || !sp || sched->n_heavy <= 0 || sp->n_pos <= 0 || sp->n_pieces <= 0 || H <= 0 ||
+      !sp->perm || !sp->starts || !sp->chunk_piece || !sp->row_ptr || !sp->row_pieces)
+    return p;
+  const size_t part = (size_t)sp->n_pieces * (size_t)H;
+  p.off_counter = (p.bytes + 255) / 256 * 256;
+  p.off_pm = p.off_counter + 256;
+  p.off_pl = (p.off_pm + part * F + 255) / 256 * 256;
+  p.bytes = p.off_pl + part * sizeof(double);
+  p.on = true;
+  return p;
+}
+
 size_t gmp_edge_softmax_workspace_size_ex(const gmp_adj* in_adj, const gmp_sched* sched, int32_t H,
                                           int dtype, int backward) {
   const size_t F = dtype == GMP_F64 ? 8 : 4;
-  return window_plan(in_adj, sched, H, F, backward != 0, softmax_vec(F, H)).bytes;
+  return std::max(window_plan(in_adj, sched, H, F, backward != 0, softmax_vec(F, H)).bytes,
+                  seg_layout(in_adj, sched, H, F).bytes);
 }
 
 static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sched* sched,
@@ -737,7 +762,48 @@ static int softmax_common(const gmp_adj* adj, const gmp_coo* coo, const gmp_sche
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   const WindowPlan wp = uv ? WindowPlan{} : window_plan(adj, sched, H, F, bwd, V);
-  if (wp.on && ntiles == 1 && V == softmax_vec(F, H) && ws_bytes >= wp.bytes) {
+  const SegLayout sgl = uv ? SegLayout{} : seg_layout(adj, sched, H, F);
+  if (sgl.on && ntiles == 1 && sched->order && ws_bytes >= sgl.bytes &&
+      sched->segplan->group == (32 >> a.g_log2) &&
+      sched->segplan->n_pos % (kSegChunkSub * sched->segplan->group) == 0 && lds < (1ll << 31) &&
+      ldg < (1ll << 31)) {
+    // heavy rows: one chunked segmented pass over the window-major plan;
+    // the rest as below
+    const gmp_segplan* sp = sched->segplan;
+    SegArgs sg{};
+    sg.perm = sp->perm;
+    sg.starts = sp->starts;
+    sg.chunk_piece = sp->chunk_piece;
+    sg.row_ptr = sp->row_ptr;
+    sg.row_pieces = sp->row_pieces;
+    sg.n_pos = sp->n_pos;
+    const int64_t chunk_pos = (int64_t)kSegChunkSub * sp->group;
+    sg.n_chunks = (sp->n_pos + chunk_pos - 1) / chunk_pos;
+    sg.n_pieces = sp->n_pieces;
+    sg.counter = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + sgl.off_counter);
+    sg.pm = static_cast<char*>(ws) + sgl.off_pm;
+    sg.pl = reinterpret_cast<double*>(static_cast<char*>(ws) + sgl.off_pl);
+    e = launch_edge_softmax_seg(F == 8, V, bwd, a, sg, st);
+    g_launches += 2;
+    const int64_t n_med = std::max(n_heavy, std::min(sched->n_medium, sched->n_nonempty));
+    SoftmaxArgs lt = a;
+    lt.order = a.order + n_heavy;
+    lt.n_rows = n_med - n_heavy;
+    lt.n_heavy = 0;
+    lt.blocks_per_tile = (lt.n_rows + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (e == cudaSuccess && lt.n_rows > 0) {
+      e = launch_edge_softmax(F == 8, V, bwd, uv, lt, lt.blocks_per_tile, st);
+      g_launches++;
+    }
+    SoftmaxArgs sl = a;
+    sl.order = a.order + n_med;
+    sl.n_rows = sched->n_nonempty - n_med;
+    sl.n_heavy = 0;
+    if (e == cudaSuccess && sl.n_rows > 0) {
+      e = launch_edge_softmax_slots(F == 8, V, bwd, uv, sl, st);
+      g_launches++;
+    }
+  } else if (wp.on && ntiles == 1 && V == softmax_vec(F, H) && ws_bytes >= wp.bytes) {
     // heavy rows: edge-id windows; the rest: the row kernel on the light rows
     WindowArgs w{};
     w.sorted_eids = sched->sorted_eids;

@@ -1,6 +1,7 @@
 // kernels_misc.cu - launchers for the dot / SDDMM / softmax kernels, the
 // extrema gradient kernels and the degree-binned schedule builder.
 #include <cub/device/device_radix_sort.cuh>
+#include <cstdlib>
 
 #include "sddmm.cuh"
 #include "softmax.cuh"
@@ -209,6 +210,62 @@ cudaError_t launch_edge_softmax_window(int f64, int V, bool bwd, const SoftmaxAr
   return cudaGetLastError();
 }
 
+template <typename T, bool BWD>
+static const void* seg_kernel_fn(int V) {
+  if constexpr (sizeof(T) == 4) {
+    if (V == 4) return (const void*)edge_softmax_seg_kernel<T, 4, BWD>;
+  }
+  if (V == 2) return (const void*)edge_softmax_seg_kernel<T, 2, BWD>;
+  return (const void*)edge_softmax_seg_kernel<T, 1, BWD>;
+}
+
+template <typename T, bool BWD>
+static void softmax_seg_v(int V, const SoftmaxArgs& a, const SegArgs& sg, unsigned grid,
+                          cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {
+    if (V == 4) { edge_softmax_seg_kernel<T, 4, BWD><<<grid, kWarpsPerCta * 32, 0, s>>>(a, sg); return; }
+  }
+  if (V == 2) { edge_softmax_seg_kernel<T, 2, BWD><<<grid, kWarpsPerCta * 32, 0, s>>>(a, sg); return; }
+  edge_softmax_seg_kernel<T, 1, BWD><<<grid, kWarpsPerCta * 32, 0, s>>>(a, sg);
+}
+
+// segmented heavy-row statistics (softmax.cuh): persistent warps claiming
+// chunks in order, then the per-row piece merge
+cudaError_t launch_edge_softmax_seg(int f64, int V, bool bwd, const SoftmaxArgs& a,
+                                    const SegArgs& sg, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(sg.counter, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fn = f64 ? (bwd ? seg_kernel_fn<double, true>(V) : seg_kernel_fn<double, false>(V))
+                       : (bwd ? seg_kernel_fn<float, true>(V) : seg_kernel_fn<float, false>(V));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kWarpsPerCta * 32, 0);
+  static const int cap = [] {
+    const char* v = getenv("GMP_SOFTMAX_SEG_CTAS");  // resident CTAs per SM (tuning)
+    return v ? std::max(1, atoi(v)) : 0;
+  }();
+  if (cap) per = std::min(per, cap);
+  const unsigned grid = (unsigned)(std::max(1, per) * sms);
+  if (f64) {
+    if (bwd) softmax_seg_v<double, true>(V, a, sg, grid, s);
+    else softmax_seg_v<double, false>(V, a, sg, grid, s);
+  } else {
+    if (bwd) softmax_seg_v<float, true>(V, a, sg, grid, s);
+    else softmax_seg_v<float, false>(V, a, sg, grid, s);
+  }
+  const int64_t total = a.n_heavy * (int64_t)a.H;  // one warp each
+  const unsigned mg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 7) / 8, 148 * 16));
+  if (f64) {
+    if (bwd) edge_softmax_seg_merge<double, true><<<mg, 256, 0, s>>>(a, sg);
+    else edge_softmax_seg_merge<double, false><<<mg, 256, 0, s>>>(a, sg);
+  } else {
+    if (bwd) edge_softmax_seg_merge<float, true><<<mg, 256, 0, s>>>(a, sg);
+    else edge_softmax_seg_merge<float, false><<<mg, 256, 0, s>>>(a, sg);
+  }
+  return cudaGetLastError();
+}
+
 template <typename T, bool BWD, bool UV>
 static void softmax_apply_v(int V, const SoftmaxArgs& a, cudaStream_t s) {
   const int64_t total = a.m * (int64_t)(a.H / V);
@@ -386,9 +443,11 @@ cudaError_t launch_extrema_bwd_copy(int f64, int64_t n, int32_t d, const int64_t
 // autodiff.py:289-372). Cell (v, k) with winner e = arg[v, k] contributes
 // dZ[v, k] * d phi / d operand, evaluated in fp64 on the winner's operands
 // (the reference's fp64 expression order), to the operand's row: src[e]
-// (several cells can hit one source row: atomicAdd), v or e (one cell per
+// (several cells can hit one source row: the cells go to a CellSink as
+// (row, column) keyed fp64 values, sorted and summed in fp64 in key order by
+// sort_and_sum - deterministic, no float atomics), v or e (one cell per
 // (row, column): plain store, bit-exact) - a broadcast operand (own_dim == 1)
-// sums its cells with atomicAdd.
+// sums its cells the same way.
 struct ExtBinArgs {
   int64_t n;
   int32_t d;

@@ -516,6 +516,276 @@ __global__ void edge_softmax_window_merge(const SoftmaxArgs a, const WindowArgs 
   }
 }
 
+// Segmented statistics for the heavy rows (edge-keyed scores; replaces the
+// (window, row) work items above when a gmp_segplan is given). The heavy
+// rows' in-edges are laid out once per graph in window-major order - edge
+// ids sorted by (eid / win, heavy row, eid) - each (window, row) segment
+// padded with -1 to a multiple of the lane-group count E, so a warp sub-step
+// (E positions, one per lane group) never straddles two segments. Pieces =
+// segments cut every kSegChunkSub sub-steps (a chunk). A warp claims chunks
+// in order (the warps in flight sweep about one window of score rows, which
+// L2 holds while each 128 B line is touched by its four edges' rows); lane
+// groups read consecutive positions (coalesced), a batch of U sub-steps is
+// loaded at once, and the piece starts inside a chunk are warp-uniform bits.
+// Batches without a piece start take the group update (one max, one
+// rescale, U exps per column); the rest a rolled per-sub-step loop that
+// closes a piece (fixed xor-tree fold, one partial per piece) at each start.
+// A merge kernel folds each row's pieces in piece (= window) order, so the
+// result is deterministic.
+constexpr int kSegChunkSub = 16;  // sub-steps per chunk (GMP_SEG_CHUNK_SUB)
+// sub-steps per load batch (Reddit H=8 backward: 8 -> 3.78 ms, 4 -> 3.96 ms)
+template <bool BWD> struct SegBatch { static constexpr int value = 8; };
+
+struct SegArgs {
+  const int32_t* perm;         // n_pos edge ids, window-major, -1 = padding
+  const uint32_t* starts;      // bit j: sub-step j starts a piece
+  const int32_t* chunk_piece;  // piece id of each chunk's first sub-step
+  const int64_t* row_ptr;      // n_heavy + 1: pieces of heavy row r
+  const int32_t* row_pieces;   // piece ids grouped by heavy row, ascending
+  int64_t n_pos, n_chunks, n_pieces;
+  unsigned long long* counter; // chunk counter (zeroed by the launcher)
+  void* pm;                    // (n_pieces, H) T: partial max (fwd)
+  double* pl;                  // (n_pieces, H): partial sum
+};
+
+// Fold of one piece across the warp's lane groups: the common maximum
+// first (order-free), then every lane group rescales its own compensated sum
+// once and a fixed xor tree adds the fp64 values (deterministic). Cheaper than
+// a pairwise online merge at each tree level (one exp per lane, no branches).
+template <typename T, int V, bool BWD>
+__device__ __forceinline__ void seg_fold(int G, T (&m)[V], const ColSum<T> (&acc)[V],
+                                         double (&l)[V]) {
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    if constexpr (BWD) {
+      l[k] = acc[k].value();
+    } else {
+      T M = m[k];
+      for (int off = G; off < 32; off <<= 1) M = fmax(M, __shfl_xor_sync(kFull, M, off));
+      l[k] = m[k] == T(-INFINITY) ? 0.0 : acc[k].value() * (double)sm_exp(m[k], M);
+      m[k] = M;
+    }
+    for (int off = G; off < 32; off <<= 1) l[k] += __shfl_xor_sync(kFull, l[k], off);
+  }
+}
+
+// packed (f32x2) column-pair updates of the batch fast path
+__device__ __forceinline__ float2 ex2_2(float2 d) {
+  const float2 y = __fmul2_rn(d, f2(kLog2e, kLog2e));
+  return f2(ex2_approx(y.x), ex2_approx(y.y));
+}
+
+template <typename T, int V, bool BWD>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    edge_softmax_seg_kernel(const SoftmaxArgs a, const SegArgs sg) {
+  constexpr int U = SegBatch<BWD>::value;
+  constexpr bool PACK = sizeof(T) == 4 && V % 2 == 0;
+  const int lane = threadIdx.x & 31;
+  const int G = 1 << a.g_log2, E = 32 >> a.g_log2;
+  const int slot = lane >> a.g_log2, gl = lane & (G - 1);
+  const int col = gl * V;
+  const bool valid = col < a.H;
+  const int ccol = valid ? col : 0;
+  const T* S = static_cast<const T*>(a.s) + ccol;
+  const T* Gd = static_cast<const T*>(a.g) + ccol;
+  const int32_t lds = (int32_t)a.lds, ldg = (int32_t)a.ldg;  // host-checked < 2^31
+  T* PM = static_cast<T*>(sg.pm);
+  const T pad = BWD ? T(0) : T(-INFINITY);  // padding: no max, exp 0 / product 0
+  T m[V];
+  ColSum<T> acc[V];
+  int64_t piece = 0;
+  auto reset = [&]() {
+#pragma unroll
+    for (int k = 0; k < V; ++k) { m[k] = -INFINITY; acc[k] = ColSum<T>(); }
+  };
+  auto flush = [&]() {
+    double l[V];
+    seg_fold<T, V, BWD>(G, m, acc, l);
+    if (slot == 0 && valid) {
+      const int64_t base = piece * a.H + col;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if constexpr (!BWD) PM[base + k] = m[k];
+        sg.pl[base + k] = l[k];
+      }
+    }
+    reset();
+  };
+  // the edge ids of the next batch are loaded one batch ahead (across chunk
+  // boundaries: the next chunk is claimed one ahead), so each batch waits for
+  // one memory latency (its score rows), not two (ids, then rows)
+  int32_t ev[U];
+  auto load_ids = [&](int64_t cc, int b) {
+    const int32_t* pp = sg.perm + (cc * kSegChunkSub + b) * E + slot;  // whole chunks
+#pragma unroll
+    for (int u = 0; u < U; ++u) ev[u] = __ldg(pp + u * E);
+  };
+  unsigned long long nxt = 0;
+  if (lane == 0) nxt = atomicAdd(sg.counter, 1ull);
+  int64_t c = (int64_t)__shfl_sync(kFull, nxt, 0);
+  if (c >= sg.n_chunks) return;
+  if (lane == 0) nxt = atomicAdd(sg.counter, 1ull);
+  load_ids(c, 0);
+  for (;;) {
+    const int64_t j0 = c * kSegChunkSub;  // first sub-step of the chunk
+    const uint32_t cb = (__ldg(sg.starts + (j0 >> 5)) >> (j0 & 31)) & ((1u << kSegChunkSub) - 1u);
+    piece = (int64_t)__ldg(sg.chunk_piece + c);  // bit 0 of cb is always set
+    reset();
+#pragma unroll 1
+    for (int b = 0; b < kSegChunkSub; b += U) {
+      T x[U][V], gg[U][V];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) { x[u][k] = pad; gg[u][k] = T(0); }
+        if (ev[u] >= 0 && valid) {
+          load_vec<T, V>(S + (int64_t)ev[u] * lds, x[u]);
+          if constexpr (BWD) load_vec<T, V>(Gd + (int64_t)ev[u] * ldg, gg[u]);
+        }
+      }
+      if (b + U < kSegChunkSub) {
+        load_ids(c, b + U);
+      } else {
+        const int64_t cn = (int64_t)__shfl_sync(kFull, nxt, 0);
+        if (cn < sg.n_chunks) load_ids(cn, 0);
+      }
+      const uint32_t bits = (cb >> b) & ((1u << U) - 1u);
+      if ((bits >> 1) == 0) {
+        // no piece start after this batch's first sub-step
+        if (b > 0 && (bits & 1u)) { flush(); ++piece; }
+        if constexpr (BWD) {
+          if constexpr (PACK) {
+#pragma unroll
+            for (int k = 0; k < V; k += 2) {
+              float2 s2 = f2(acc[k].s, acc[k + 1].s), c2 = f2(acc[k].c, acc[k + 1].c);
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const float2 xx = f2(x[u][k], x[u][k + 1]), yy = f2(gg[u][k], gg[u][k + 1]);
+                const float2 pr = __fmul2_rn(xx, yy);
+                two_sum2(s2, c2, pr);
+                c2 = __fadd2_rn(c2, __ffma2_rn(xx, yy, f2(-pr.x, -pr.y)));
+              }
+              acc[k].s = s2.x; acc[k + 1].s = s2.y; acc[k].c = c2.x; acc[k + 1].c = c2.y;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+#pragma unroll
+              for (int u = 0; u < U; ++u) acc[k].add_prod(x[u][k], gg[u][k]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            T mx = m[k];
+#pragma unroll
+            for (int u = 0; u < U; ++u) mx = fmax(mx, x[u][k]);
+            if (mx > m[k]) {
+              if (m[k] != T(-INFINITY)) acc[k].scale(sm_exp(m[k], mx));
+              m[k] = mx;
+            }
+          }
+          if constexpr (PACK) {
+#pragma unroll
+            for (int k = 0; k < V; k += 2) {
+              if (m[k] == T(-INFINITY) || m[k + 1] == T(-INFINITY)) {  // padding / -inf scores
+#pragma unroll
+                for (int h = k; h < k + 2; ++h) {
+                  if (m[h] == T(-INFINITY)) continue;
+#pragma unroll
+                  for (int u = 0; u < U; ++u) acc[h].add(sm_exp(x[u][h], m[h]));
+                }
+                continue;
+              }
+              float2 s2 = f2(acc[k].s, acc[k + 1].s), c2 = f2(acc[k].c, acc[k + 1].c);
+              const float2 m2 = f2(m[k], m[k + 1]);
+#pragma unroll
+              for (int u = 0; u < U; ++u) two_sum2(s2, c2, ex2_2(fsub2(f2(x[u][k], x[u][k + 1]), m2)));
+              acc[k].s = s2.x; acc[k + 1].s = s2.y; acc[k].c = c2.x; acc[k + 1].c = c2.y;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              if (m[k] == T(-INFINITY)) continue;
+#pragma unroll
+              for (int u = 0; u < U; ++u) acc[k].add(sm_exp(x[u][k], m[k]));
+            }
+          }
+        }
+      } else {
+        // rolled: one sub-step per iteration, the batch shifted down a slot
+#pragma unroll 1
+        for (int u = 0; u < U; ++u) {
+          if (((bits >> u) & 1u) && (b > 0 || u > 0)) { flush(); ++piece; }
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            if constexpr (BWD) {
+              acc[k].add_prod(x[0][k], gg[0][k]);
+            } else if (x[0][k] != T(-INFINITY)) {
+              if (x[0][k] > m[k]) {
+                if (m[k] != T(-INFINITY)) acc[k].scale(sm_exp(m[k], x[0][k]));
+                m[k] = x[0][k];
+              }
+              acc[k].add(sm_exp(x[0][k], m[k]));
+            }
+          }
+#pragma unroll
+          for (int w = 0; w + 1 < U; ++w) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) { x[w][k] = x[w + 1][k]; gg[w][k] = gg[w + 1][k]; }
+          }
+        }
+      }
+    }
+    flush();  // pieces never cross a chunk boundary
+    c = (int64_t)__shfl_sync(kFull, nxt, 0);
+    if (c >= sg.n_chunks) return;
+    if (lane == 0) nxt = atomicAdd(sg.counter, 1ull);
+  }
+}
+
+// one warp per (heavy row, column): lanes fold strided pieces of the row in
+// piece order, then a fixed xor tree combines the lanes (deterministic)
+template <typename T, bool BWD>
+__global__ void edge_softmax_seg_merge(const SoftmaxArgs a, const SegArgs sg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = a.n_heavy * (int64_t)a.H;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T* PM = static_cast<const T*>(sg.pm);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nw) {
+    const int64_t r = i / a.H;
+    const int c = (int)(i - r * a.H);
+    const int64_t q0 = sg.row_ptr[r], q1 = sg.row_ptr[r + 1];
+    T mm = -INFINITY;
+    double ll = 0.0;
+    for (int64_t q = q0 + lane; q < q1; q += 32) {
+      const int64_t at = (int64_t)__ldg(sg.row_pieces + q) * a.H + c;
+      if constexpr (BWD) ll += sg.pl[at];
+      else sm_merge<T>(mm, ll, PM[at], sg.pl[at]);
+    }
+    for (int off = 1; off < 32; off <<= 1) {
+      const double ol = __shfl_xor_sync(kFull, ll, off);
+      if constexpr (BWD) {
+        ll += ol;
+      } else {
+        const T om = __shfl_xor_sync(kFull, mm, off);
+        sm_merge<T>(mm, ll, om, ol);
+      }
+    }
+    if (lane != 0) continue;
+    const int64_t row = a.order[r];
+    T* st = static_cast<T*>(a.stat) + row * 2 * (int64_t)a.H + c;
+    if constexpr (BWD) {
+      const T hi = (T)ll;
+      st[0] = hi;
+      st[a.H] = (T)(ll - (double)hi);
+    } else {
+      st[0] = mm;
+      st[a.H] = (T)(1.0 / ll);
+    }
+  }
+}
+
 // alpha[e] = exp(s[e] - max[dst e]) * inv_sum[dst e]   (fwd)
 // ds[e]    = alpha[e] * (g[e] - sum[dst e])            (bwd)
 // Edge-id order: s / g / alpha / ds stream coalesced; the per-destination
@@ -618,5 +888,7 @@ cudaError_t launch_edge_softmax_window(int dtype_is_f64, int V, bool bwd, const 
                                        const WindowArgs& w, cudaStream_t s);
 cudaError_t launch_edge_softmax_apply(int dtype_is_f64, int V, bool bwd, bool uv,
                                       const SoftmaxArgs& a, cudaStream_t s);
+cudaError_t launch_edge_softmax_seg(int dtype_is_f64, int V, bool bwd, const SoftmaxArgs& a,
+                                    const SegArgs& sg, cudaStream_t s);
 
 }  // namespace gmp

@@ -844,18 +844,132 @@ def _sorted_eids(adj):
     return se
 
 
+# sub-steps per chunk of the segmented statistics pass (GMP_SEG_CHUNK_SUB, gmp.h)
+_SEG_CHUNK_SUB = 16
+# L2 bytes one window of score rows (both operands in the backward) may take
+_SEG_WINDOW_MB = int(os.environ.get("GMP_SOFTMAX_SEG_MB", "64"))
+# GMP_SOFTMAX_SEG=0 keeps the (window, row) work-item kernel (measurements)
+_SEG_OFF = os.environ.get("GMP_SOFTMAX_SEG", "1") in ("", "0")
+# the backward's statistics (two score arrays per edge) keep the (window, row)
+# item kernel: measured Reddit H=8 3.68 ms vs 3.78 ms segmented (GMP_SOFTMAX_SEG_BWD=1)
+_SEG_BWD_OFF = os.environ.get("GMP_SOFTMAX_SEG_BWD", "0") in ("", "0")
+# below this many edges the score rows fit L2 and the row walk is as good
+_SEG_MIN_EDGES = 1 << 22
+
+
+class _Segplan:
+    pass
+
+
+def _softmax_lane_groups(H, itemsize, ld_ok=True):
+    """Lane groups per warp of the softmax kernels for H heads (gmp_api.cu
+    softmax_vec / pick_v with aligned operands): V elements per lane,
+    next_pow2(H / V) lanes per score row."""
+    if itemsize == 4 and H % 4 == 0:
+        v = 4
+    elif H % 2 == 0:
+        v = 2
+    else:
+        v = 1
+    lanes = 1
+    while lanes < -(-H // v):
+        lanes *= 2
+    return 32 // min(lanes, 32)
+
+
+def _softmax_segplan(adj, sched, win, group):
+    """Window-major piece layout of the heavy rows' in-edges (gmp_segplan,
+    gmp.h), cached per (window, lane groups). The heavy rows' edge ids sorted
+    by (eid // win, heavy row index, eid), each (window, row) segment padded
+    with -1 to a multiple of `group` positions (one warp sub-step); pieces =
+    segments cut every _SEG_CHUNK_SUB sub-steps; row_pieces groups the piece
+    ids by heavy row in ascending (= window) order. Built once with device
+    sorts."""
+    key = ("segplan", int(win), int(group))
+    plan = adj._extra.get(key)
+    if plan is not None:
+        return plan
+    R = sched.n_heavy
+    dev = adj.indptr.device
+    rows = sched.order[:R].to(torch.int64)
+    first = adj.indptr.index_select(0, rows)
+    deg = adj.indptr.index_select(0, rows + 1) - first
+    n_edges = int(deg.sum())
+    r_of = torch.repeat_interleave(torch.arange(R, device=dev), deg)
+    base = torch.cumsum(deg, 0) - deg
+    pos = torch.arange(n_edges, device=dev) - base.index_select(0, r_of) + first.index_select(0, r_of)
+    eid = _sorted_eids(adj).index_select(0, pos)
+    del pos, base
+    wkey = torch.div(eid, int(win), rounding_mode="floor").to(torch.int64) * R + r_of
+    del r_of
+    wkey, idx = torch.sort(wkey, stable=True)
+    eid = eid.index_select(0, idx)
+    del idx
+    # segments (runs of one (window, row)) and their padded extents
+    seg_keys, seg_len = torch.unique_consecutive(wkey, return_counts=True)
+    del wkey
+    seg_sub = -(-seg_len // group)                      # sub-steps per segment
+    seg_start = torch.cumsum(seg_len, 0) - seg_len      # unpadded first position
+    seg_sub_start = torch.cumsum(seg_sub, 0) - seg_sub  # first sub-step
+    n_sub = -(-int(seg_sub.sum()) // _SEG_CHUNK_SUB) * _SEG_CHUNK_SUB  # whole chunks
+    n_pos = n_sub * group
+    seg_of = torch.repeat_interleave(torch.arange(seg_keys.numel(), device=dev), seg_len)
+    dest = (torch.arange(n_edges, device=dev) - seg_start.index_select(0, seg_of)
+            + seg_sub_start.index_select(0, seg_of) * group)
+    del seg_of, seg_start
+    perm = torch.full((n_pos,), -1, dtype=torch.int32, device=dev)
+    perm[dest] = eid
+    del dest, eid
+    # piece starts per sub-step: a segment's first sub-step or a chunk start
+    new = torch.zeros(n_sub, dtype=torch.bool, device=dev)
+    new[seg_sub_start] = True
+    new[::_SEG_CHUNK_SUB] = True
+    pid = torch.cumsum(new, 0)
+    n_pieces = int(pid[-1])
+    chunk_piece = (pid[::_SEG_CHUNK_SUB] - 1).to(torch.int32)
+    sub_seg = torch.repeat_interleave(torch.arange(seg_keys.numel(), device=dev), seg_sub)
+    tail = n_sub - sub_seg.numel()  # padding sub-steps of the last chunk: last segment's
+    if tail:
+        sub_seg = torch.cat([sub_seg, sub_seg[-1:].expand(tail)])
+    piece_row = torch.remainder(seg_keys.index_select(0, sub_seg[new]), R)
+    del pid, sub_seg
+    row_pieces = torch.sort(piece_row, stable=True).indices.to(torch.int32)
+    row_ptr = torch.zeros(R + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(torch.bincount(piece_row, minlength=R), 0, out=row_ptr[1:])
+    nw = -(-n_sub // 32)
+    bits = torch.zeros(nw * 32, dtype=torch.int64, device=dev)
+    bits[:n_sub] = new.to(torch.int64)
+    words = (bits.view(nw, 32) << torch.arange(32, device=dev)).sum(1)
+    starts = torch.where(words >= 2 ** 31, words - 2 ** 32, words).to(torch.int32)
+    plan = _Segplan()
+    plan.tensors = (perm, starts, chunk_piece, row_ptr, row_pieces)
+    plan.struct = _lib.GmpSegplan(n_pos, n_pieces, int(win), int(group), perm.data_ptr(),
+                                  starts.data_ptr(), chunk_piece.data_ptr(), row_ptr.data_ptr(),
+                                  row_pieces.data_ptr())
+    adj._extra[key] = plan
+    return plan
+
+
 def _softmax_call(g, fn_name, S, G2, H, out, what):
     lib = _lib.load()
     adj = g.to_csc()
     sched = adj.schedule()
     if sched.n_heavy and g.num_edges >= (1 << 22) and not sched.struct.sorted_eids:
         sched.struct.sorted_eids = _sorted_eids(adj).data_ptr()
+    sc = sched.struct
+    if (sched.n_heavy and g.num_edges >= _SEG_MIN_EDGES and not _SEG_OFF
+            and not (G2 is not None and _SEG_BWD_OFF)):
+        row_bytes = H * S.element_size() * (2 if G2 is not None else 1)
+        plan = _softmax_segplan(adj, sched, max(1 << 10, (_SEG_WINDOW_MB << 20) // row_bytes),
+                                _softmax_lane_groups(H, S.element_size()))
+        sc = _lib.GmpSched.from_buffer_copy(sched.struct)
+        sc.segplan = ctypes.addressof(plan.struct)
     ws_bytes = int(lib.gmp_edge_softmax_workspace_size_ex(
-        ctypes.byref(_adj_struct(adj)), ctypes.byref(sched.struct), H, _dtype_code(S),
+        ctypes.byref(_adj_struct(adj)), ctypes.byref(sc), H, _dtype_code(S),
         1 if G2 is not None else 0))
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=g.device)
     coo = _lib.GmpCoo(g.num_nodes, g.num_edges, g.src.data_ptr(), g.dst.data_ptr())
-    args = [ctypes.byref(_adj_struct(adj)), ctypes.byref(coo), ctypes.byref(sched.struct),
+    args = [ctypes.byref(_adj_struct(adj)), ctypes.byref(coo), ctypes.byref(sc),
             _dtype_code(S), S.data_ptr(), _ld(S)]
     if G2 is not None:
         args += [G2.data_ptr(), _ld(G2)]

@@ -137,3 +137,24 @@ def test_round1_entry_points_validate_without_gpu():
     # windowed softmax workspace: no schedule -> the plain size
     assert lib.gmp_edge_softmax_workspace_size_ex(ctypes.byref(adj), None, 8, 0, 0) == \
         lib.gmp_edge_softmax_workspace_size(3, 8)
+
+
+def test_segplan_workspace_size():
+    """gmp_edge_softmax_workspace_size_ex with a gmp_segplan in the schedule
+    reserves the per-piece partials ((max, sum) per head) after the per-row
+    statistics; a plan without arrays is ignored (pure size arithmetic, no
+    device access)."""
+    lib = _lib.load()
+    adj = _lib.GmpAdj(3, 5, None, None, None)
+    plan = _lib.GmpSegplan(256, 1000, 4096, 16, 1, 1, 1, 1, 1)
+    sched = _lib.GmpSched()
+    sched.n_heavy = 1
+    sched.segplan = ctypes.addressof(plan)
+    base = lib.gmp_edge_softmax_workspace_size(3, 8)
+    for dtype, F in ((0, 4), (1, 8)):
+        got = lib.gmp_edge_softmax_workspace_size_ex(ctypes.byref(adj), ctypes.byref(sched), 8,
+                                                     dtype, 0)
+        assert got >= base + 256 + 1000 * 8 * (F + 8)
+    plan.perm = None
+    assert lib.gmp_edge_softmax_workspace_size_ex(ctypes.byref(adj), ctypes.byref(sched), 8, 0,
+                                                  0) == base
