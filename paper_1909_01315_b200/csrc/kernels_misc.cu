@@ -243,7 +243,7 @@ cudaError_t launch_edge_softmax_seg(int f64, int V, bool bwd, const SoftmaxArgs&
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kWarpsPerCta * 32, 0);
   static const int cap = [] {
     const char* v = getenv("GMP_SOFTMAX_SEG_CTAS");  // resident CTAs per SM (tuning)
-    return v ? std::max(1, atoi(v)) : 0;
+    return v ? std::max(0, atoi(v)) : 0;  // 0 / unset: occupancy limit only
   }();
   if (cap) per = std::min(per, cap);
   const unsigned grid = (unsigned)(std::max(1, per) * sms);
