@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 #pragma unroll
               for (int u = 0; u < U; ++u) {
                 const float2 xx = f2(x[u][k], x[u][k + 1]), yy = f2(gg[u][k], gg[u][k + 1]);
-                const float2 pr = __fmul2_rn(xx, yy);
+                const float2 pr = fmul2(xx, yy);
                 two_sum2(s2, c2, pr);
                 c2 = __fadd2_rn(c2, __ffma2_rn(xx, yy, f2(-pr.x, -pr.y)));
               }

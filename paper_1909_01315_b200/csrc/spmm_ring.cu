@@ -91,14 +91,10 @@ struct Comp4 {
     if constexpr (OP == OP_COPY) {
       two_sum2(s0, c0, f2(v.x, v.y));
       two_sum2(s1, c1, f2(v.z, v.w));
-    } else {  // x * w = pr + fma(x, w, -pr) exactly
+    } else {  // the row kernel's product accumulate (two_sum_prod2)
       const float2 ww = f2(w, w);
-      const float2 x0 = f2(v.x, v.y), x1 = f2(v.z, v.w);
-      const float2 pr0 = __fmul2_rn(x0, ww), pr1 = __fmul2_rn(x1, ww);
-      two_sum2(s0, c0, pr0);
-      two_sum2(s1, c1, pr1);
-      c0 = __fadd2_rn(c0, __ffma2_rn(x0, ww, f2(-pr0.x, -pr0.y)));
-      c1 = __fadd2_rn(c1, __ffma2_rn(x1, ww, f2(-pr1.x, -pr1.y)));
+      two_sum_prod2(s0, c0, f2(v.x, v.y), ww);
+      two_sum_prod2(s1, c1, f2(v.z, v.w), ww);
     }
   }
   __device__ __forceinline__ void fold(double (&acc)[4]) {

@@ -266,13 +266,57 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   return *reinterpret_cast<float2*>(&r);
 }
 
+// x * y on packed fp32x2 as its own rounded FMUL2 (with fadd2 below: a
+// product contracted into the following add breaks TwoSum's premise that
+// the addend is a float)
+// ptxas fuses mul.rn.f32x2 into a following add.rn.f32x2 (FFMA2 in the
+// SASS, contrary to the .rn no-contraction rule), so the rounded product is
+// formed by two scalar FMULs, which it keeps
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
+
+// a + b as its own rounded FADD2: ptxas contracts __fadd2_rn(s, x * y) into
+// an FFMA2 even when the product comes from mul.rn.f32x2 (seen in the SASS)
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
 // s + c += x exactly (TwoSum, Knuth); packed fp32x2, seven FADD2.
 __device__ __forceinline__ void two_sum2(float2& s, float2& c, float2 x) {
-  const float2 t = __fadd2_rn(s, x);
+  const float2 t = fadd2(s, x);  // never contracted with a producer of x
   const float2 bb = fsub2(t, s);               // t - s
   const float2 e1 = fsub2(s, fsub2(t, bb));    // s - (t - bb)
   const float2 e2 = fsub2(x, bb);              // x - bb
   c = __fadd2_rn(c, __fadd2_rn(e1, e2));
+  s = t;
+}
+
+// s + x*y accumulated exactly to second order: TwoSum of the rounded product
+// pr with its two error parts fused - (pr - bb) + (x*y - pr) = x*y - bb in
+// one FMA (rounded once, 2^-24 of a term already ~2^-24 of |t|) - 8 packed
+// ops per column pair instead of TwoProduct + TwoSum's 10
+__device__ __forceinline__ void two_sum_prod2(float2& s, float2& c, float2 x, float2 y) {
+  const float2 pr = fmul2(x, y);
+  const float2 t = fadd2(s, pr);
+  const float2 bb = fsub2(t, s);                        // t - s
+  const float2 e1 = fsub2(s, fsub2(t, bb));             // s - (t - bb)
+  const float2 e2 = __ffma2_rn(x, y, f2(-bb.x, -bb.y));  // x*y - bb
+  c = __fadd2_rn(c, __fadd2_rn(e1, e2));
+  s = t;
+}
+__device__ __forceinline__ void two_sum_prod1(float& s, float& c, float x, float y) {
+  const float pr = __fmul_rn(x, y);
+  const float t = __fadd_rn(s, pr);
+  const float bb = __fsub_rn(t, s);
+  const float e1 = __fsub_rn(s, __fsub_rn(t, bb));
+  const float e2 = __fmaf_rn(x, y, -bb);
+  c = __fadd_rn(c, __fadd_rn(e1, e2));
   s = t;
 }
 
@@ -329,9 +373,7 @@ struct RowAcc {
         if constexpr (OP == OP_COPY) {
           two_sum1(s[0], c[0], x);
         } else if constexpr (OP == OP_MUL || OP == OP_DOT) {
-          const float pr = __fmul_rn(x, y);
-          two_sum1(s[0], c[0], pr);
-          c[0] = __fadd_rn(c[0], __fmaf_rn(x, y, -pr));
+          two_sum_prod1(s[0], c[0], x, y);
         } else {  // ADD / SUB: the exact message is itself a TwoSum pair
           const float yy = OP == OP_SUB ? -y : y;
           const float t = __fadd_rn(x, yy);
@@ -348,10 +390,7 @@ struct RowAcc {
           if constexpr (OP == OP_COPY) {
             two_sum2(S, C, x);
           } else if constexpr (OP == OP_MUL || OP == OP_DOT) {
-            const float2 y = f2((float)b[k], (float)b[k + 1]);
-            const float2 pr = __fmul2_rn(x, y);
-            two_sum2(S, C, pr);
-            C = __fadd2_rn(C, __ffma2_rn(x, y, f2(-pr.x, -pr.y)));
+            two_sum_prod2(S, C, x, f2((float)b[k], (float)b[k + 1]));
           } else {
             float2 y = f2((float)b[k], (float)b[k + 1]);
             if constexpr (OP == OP_SUB) y = f2(-y.x, -y.y);
