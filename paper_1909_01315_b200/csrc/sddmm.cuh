@@ -136,9 +136,7 @@ __global__ void __launch_bounds__(256) sddmm_dot_lane_kernel(const SddmmArgs a) 
 #pragma unroll
         for (int k = 0; k < V; k += 2) {
           const float2 x = f2(xa[k], xa[k + 1]), y = f2(xb[k], xb[k + 1]);
-          const float2 pr = fmul2(x, y);
-          two_sum2(S, C, pr);
-          C = __fadd2_rn(C, __ffma2_rn(x, y, f2(-pr.x, -pr.y)));
+          two_sum_prod2(S, C, x, y);  // spmm_rows.cuh: exact products, no contraction
         }
       }
       r = ((double)S.x + (double)S.y) + ((double)C.x + (double)C.y);
