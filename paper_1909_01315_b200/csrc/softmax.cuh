@@ -78,11 +78,7 @@ template <typename T> struct ColSum;
 template <> struct ColSum<float> {
   float s = 0.f, c = 0.f;
   __device__ __forceinline__ void add(float x) { two_sum1(s, c, x); }
-  __device__ __forceinline__ void add_prod(float x, float y) {
-    const float p = __fmul_rn(x, y);
-    two_sum1(s, c, p);
-    c = __fadd_rn(c, __fmaf_rn(x, y, -p));
-  }
+  __device__ __forceinline__ void add_prod(float x, float y) { two_sum_prod1(s, c, x, y); }
   __device__ __forceinline__ void scale(float f) { s = __fmul_rn(s, f); c = __fmul_rn(c, f); }
   __device__ __forceinline__ double value() const { return (double)s + (double)c; }
 };
