@@ -481,7 +481,8 @@ static int gspmm_impl(const gmp_adj* adj, const gmp_sched* sched, int op, int rh
   // light rows (degree <= the schedule's light threshold) share a warp, one
   // per lane group, in the narrow kernels and in the pipelined 256 B-row
   // kernel (launch_spmm_rows_t picks it by the same predicate)
-  const bool pipe = F == 4 && pipe_launch(V, krho, kop, mp, a.g_log2, a.need_eid);
+  const bool pipe = F == 4 && pipe_launch(V, krho, kop, mp, a.g_log2, a.need_eid,
+                                          !a.lhs.from_eid && !a.lhs.from_pos);
   const int64_t n_medium =
       (order && (narrow || pipe)) ? std::max(n_heavy, sched->n_medium) : adj->n_rows;
   const int64_t medium_blocks = (n_medium - n_heavy + kWarpsPerCta - 1) / kWarpsPerCta;

@@ -1340,9 +1340,12 @@ cudaError_t launch_rows_cfg(Kern kern, const SpmmArgs& a, int64_t grid, size_t s
 // (MP_AF / MP_AB) with one float4 per lane and 4, 8 or 16 lanes per edge
 // (64 / 128 / 256 B rows), no edge ids. The host sizes the grid by the same
 // predicate (light rows several per warp). GMP_NO_PIPE=1 disables it.
-inline bool pipe_launch(int V, int rho, int op, int mp, int g_log2, int need_eid) {
+// lhs_by_nb: the gathered operand is keyed by the neighbour (source) id -
+// the pipelined ring gathers rows by `indices` only (an edge-keyed copy
+// operand, max / min of copy_lhs(edge), takes the row kernel)
+inline bool pipe_launch(int V, int rho, int op, int mp, int g_log2, int need_eid, bool lhs_by_nb) {
   static const bool off = getenv("GMP_NO_PIPE") != nullptr;
-  if (off || V != 4 || g_log2 < 2 || g_log2 > 4) return false;
+  if (off || !lhs_by_nb || V != 4 || g_log2 < 2 || g_log2 > 4) return false;
   if (rho != RHO_SUM)  // max / min of copy_u: edge ids only for the arg
     return op == OP_COPY && mp == MP_F;
   return !need_eid && ((op == OP_COPY && mp == MP_F) ||
@@ -1355,7 +1358,7 @@ cudaError_t launch_spmm_rows_t(const SpmmArgs& a, int64_t grid, cudaStream_t s) 
                 ((OP == OP_COPY && MP == MP_F) ||
                  (RHO == RHO_SUM && OP == OP_MUL &&
                   (MP == MP_FS || MP == MP_AF || MP == MP_AB)))) {
-    if (pipe_launch(V, RHO, OP, MP, a.g_log2, a.need_eid)) {
+    if (pipe_launch(V, RHO, OP, MP, a.g_log2, a.need_eid, !a.lhs.from_eid && !a.lhs.from_pos)) {
       if (a.g_log2 == 4)
         return launch_rows_cfg(spmm_rows_kernel<T, OP, RHO, V, MP, false, 4>, a, grid, 0, s);
       if (a.g_log2 == 3)

@@ -332,3 +332,27 @@ def test_native_library_is_what_runs():
     G.gspmm(g, kernels.copy("src"), "sum", X=torch.ones(3, 2, device=DEV))
     G.gsddmm(g, kernels.copy("src"), X=torch.ones(3, 2, device=DEV))
     assert _lib.launch_count() >= before + 2
+
+
+@pytest.mark.parametrize("d", [4, 16, 32, 64])
+def test_edge_operand_extrema_medium_rows(d):
+    """max / min of copy_lhs(edge) (and of an edge-keyed binary message) on a
+    power-law graph whose medium and heavy rows take the 256 B-row kernels:
+    the operand is gathered by edge id, never by the neighbour id the
+    pipelined copy_u ring uses (C5 sweep regression: rows of degree >= 33
+    returned the extrema of the wrong rows at d = 16 / 32 / 64)."""
+    s, dd, g = _power_law_graph(60000, 20, 0)
+    n = 60000
+    rng = np.random.default_rng(d)
+    w = (np.abs(rng.standard_normal((s.size, d))) + 0.5).astype(np.float32)
+    x = (np.abs(rng.standard_normal((n, d))) + 0.5).astype(np.float32)
+    adj = O.csc(s, dd, n)
+    wt, xt = torch.as_tensor(w, device=DEV), torch.as_tensor(x, device=DEV)
+    for phi, kw, kwo in ((kernels.copy("edge"), {"W": wt}, ("copy_lhs", "edge", None, {"W": w})),
+                         (kernels.mul("src", "edge"), {"X": xt, "W": wt},
+                          ("mul", "src", "edge", {"X": x, "W": w}))):
+        for rho in ("max", "min"):
+            z, aux = G.gspmm(g, phi, rho, **kw)
+            want, waux = O.gspmm(s, dd, n, kwo[0], kwo[1], kwo[2], rho, adj=adj, workers=8, **kwo[3])
+            assert np.array_equal(to_np(z), want.astype(np.float32)), (d, phi.describe(), rho)
+            assert np.array_equal(to_np(aux.arg_edge), waux), (d, phi.describe(), rho)
